@@ -1,0 +1,397 @@
+// capi.cu -- the C ABI (include/xqr_b200.h): contexts, device workspace,
+// host<->device staging, argument validation with the reference's error
+// conventions, and kernel dispatch.  No CPU fallback: without a usable CUDA
+// device every entry point returns XQR_CUDA.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "xqr_internal.h"
+
+struct xqr_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // device arena (grown on demand, reused across calls)
+    void* arena = nullptr;
+    size_t arena_bytes = 0;
+    // pinned host staging
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool timed = false;
+    int64_t launches = 0;
+    std::string last_error;
+};
+
+namespace {
+
+int set_cuda_error(xqr_ctx* ctx, cudaError_t e, const char* where) {
+    if (ctx) ctx->last_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return XQR_CUDA;
+}
+
+void fill_status(xqr_status* st, int code, int column = 0, int64_t system = 0) {
+    if (st) {
+        st->code = code;
+        st->column = column;
+        st->system = system;
+    }
+}
+
+int fail(xqr_ctx* ctx, xqr_status* st, int code, const char* what) {
+    if (ctx) ctx->last_error = what;
+    fill_status(st, code);
+    return code;
+}
+
+bool valid_limbs(int l) { return l == 1 || l == 2 || l == 4; }
+
+// Bump allocator over the ctx arena.  Every region is 256-byte aligned.
+struct arena_plan {
+    std::vector<size_t> sizes;
+    size_t total = 0;
+    size_t add(size_t bytes) {
+        size_t off = total;
+        total += (bytes + 255) & ~size_t(255);
+        sizes.push_back(bytes);
+        return off;
+    }
+};
+
+cudaError_t ensure_arena(xqr_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->arena_bytes) return cudaSuccess;
+    if (ctx->arena) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(ctx->arena);
+        ctx->arena = nullptr;
+        ctx->arena_bytes = 0;
+    }
+    size_t want = bytes + bytes / 4;
+    cudaError_t e = cudaMalloc(&ctx->arena, want);
+    if (e != cudaSuccess) return e;
+    ctx->arena_bytes = want;
+    return cudaSuccess;
+}
+
+cudaError_t ensure_pinned(xqr_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->pinned_bytes) return cudaSuccess;
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    ctx->pinned_bytes = 0;
+    size_t want = bytes + bytes / 4;
+    cudaError_t e = cudaMallocHost(&ctx->pinned, want);
+    if (e != cudaSuccess) return e;
+    ctx->pinned_bytes = want;
+    return cudaSuccess;
+}
+
+char* at(xqr_ctx* ctx, size_t off) { return static_cast<char*>(ctx->arena) + off; }
+
+int first_code(const std::vector<xqr_status>& st) {
+    for (const auto& s : st)
+        if (s.code) return s.code;
+    return 0;
+}
+
+// Validate the shapes the reference validates (matrix.hpp:15-19: rows >= cols
+// >= 1) plus this build's size envelope.
+int check_shape(xqr_ctx* ctx, xqr_status* st, int limbs, int64_t batch, int64_t m, int64_t n) {
+    if (!valid_limbs(limbs)) return fail(ctx, st, XQR_USAGE, "limbs must be 1, 2 or 4");
+    if (n < 1 || m < n) return fail(ctx, st, XQR_DIMENSION, "matrix shape must satisfy rows >= cols >= 1");
+    if (batch < 0) return fail(ctx, st, XQR_USAGE, "negative batch");
+    if (m > 32 * xb::kMaxRowsPerLane)
+        return fail(ctx, st, XQR_USAGE, "rows > 1024 not supported by this build");
+    if (batch > 0x7fffffff) return fail(ctx, st, XQR_USAGE, "batch too large");
+    return 0;
+}
+
+// Device-side solve on device pointers (shared by host and device entry points).
+int solve_device(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t m, int64_t n,
+                 const double* d_a, const double* d_b, double* d_q, double* d_r, double* d_x,
+                 double* d_z, xqr_status* d_st, size_t scratch_off, bool timed) {
+    const int ncol = (int)n + (lsq ? 1 : 0);
+    xb::SolveParams p{};
+    p.batch = batch;
+    p.m = (int)m;
+    p.n = (int)n;
+    p.a = d_a;
+    p.b = d_b;
+    p.q = d_q;
+    p.r = d_r;
+    p.x = d_x;
+    p.z = d_z;
+    p.st = d_st;
+    p.ws_stride = xb::ws_doubles(limbs, (int)m, ncol);
+    p.rws_stride = lsq ? xb::rws_doubles(limbs, (int)n) : 0;
+    size_t need = scratch_off + sizeof(double) * (size_t)batch * (p.ws_stride + p.rws_stride) + 512;
+    cudaError_t e = ensure_arena(ctx, need);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
+    p.ws = reinterpret_cast<double*>(at(ctx, scratch_off));
+    p.rws = lsq ? p.ws + (size_t)batch * p.ws_stride : nullptr;
+    if (batch == 0) return 0;
+    if (timed) cudaEventRecord(ctx->ev0, ctx->stream);
+    e = xb::launch_mgs_cta(limbs, lsq, p, ctx->stream);
+    if (timed) cudaEventRecord(ctx->ev1, ctx->stream);
+    ctx->timed = timed;
+    ctx->launches += 1;
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "mgs kernel launch");
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int xqr_version(void) { return 100; }
+
+int xqr_ctx_create(int device, xqr_ctx** out) {
+    if (!out) return XQR_USAGE;
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        std::fprintf(stderr, "xqr_b200: no CUDA device available (%s)\n", cudaGetErrorString(e));
+        return XQR_CUDA;
+    }
+    if (device < 0 || device >= count) return XQR_USAGE;
+    e = cudaSetDevice(device);
+    if (e != cudaSuccess) return XQR_CUDA;
+    auto* ctx = new xqr_ctx();
+    ctx->device = device;
+    e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return XQR_CUDA;
+    }
+    ctx->own_stream = true;
+    cudaEventCreate(&ctx->ev0);
+    cudaEventCreate(&ctx->ev1);
+    *out = ctx;
+    return XQR_OK;
+}
+
+void xqr_ctx_destroy(xqr_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->arena) cudaFree(ctx->arena);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int xqr_ctx_set_stream(xqr_ctx* ctx, void* cuda_stream) {
+    if (!ctx) return XQR_USAGE;
+    if (!cuda_stream) return XQR_OK;
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+    ctx->own_stream = false;
+    return XQR_OK;
+}
+
+void* xqr_ctx_stream(xqr_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int xqr_ctx_synchronize(xqr_ctx* ctx) {
+    if (!ctx) return XQR_USAGE;
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? XQR_OK : set_cuda_error(ctx, e, "synchronize");
+}
+
+const char* xqr_ctx_last_error(xqr_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "no ctx"; }
+
+int64_t xqr_ctx_launch_count(xqr_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+float xqr_ctx_last_kernel_ms(xqr_ctx* ctx) {
+    if (!ctx || !ctx->timed) return 0.f;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) != cudaSuccess) return 0.f;
+    return ms;
+}
+
+// ---- device entry points -------------------------------------------------------
+int xqr_mgs_qr_batched_device(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                              const double* d_a, double* d_q, double* d_r, xqr_status* d_st) {
+    if (!ctx) return XQR_USAGE;
+    if (int c = check_shape(ctx, nullptr, limbs, batch, m, n)) return c;
+    cudaSetDevice(ctx->device);
+    return solve_device(ctx, false, limbs, batch, m, n, d_a, nullptr, d_q, d_r, nullptr, nullptr,
+                        d_st, 0, true);
+}
+
+int xqr_lsq_solve_batched_device(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                                 const double* d_a, const double* d_b, double* d_x, double* d_z,
+                                 xqr_status* d_st) {
+    if (!ctx) return XQR_USAGE;
+    if (int c = check_shape(ctx, nullptr, limbs, batch, m, n)) return c;
+    cudaSetDevice(ctx->device);
+    return solve_device(ctx, true, limbs, batch, m, n, d_a, d_b, nullptr, nullptr, d_x, d_z, d_st, 0,
+                        true);
+}
+
+int xqr_back_substitute_batched_device(xqr_ctx* ctx, int limbs, int64_t batch, int64_t n,
+                                       const double* d_r, const double* d_y, double* d_x,
+                                       xqr_status* d_st) {
+    if (!ctx) return XQR_USAGE;
+    if (!valid_limbs(limbs)) return fail(ctx, nullptr, XQR_USAGE, "limbs must be 1, 2 or 4");
+    if (n < 1) return fail(ctx, nullptr, XQR_DIMENSION, "empty triangular factor");
+    cudaSetDevice(ctx->device);
+    size_t prep = sizeof(double) * (size_t)batch * n * (3 * limbs + 1);
+    cudaError_t e = ensure_arena(ctx, prep + 256);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
+    if (batch == 0) return 0;
+    xb::BackSubParams p{batch, (int)n, d_r, d_y, d_x, d_st, reinterpret_cast<double*>(ctx->arena)};
+    cudaEventRecord(ctx->ev0, ctx->stream);
+    e = xb::launch_back_substitute(limbs, p, ctx->stream);
+    cudaEventRecord(ctx->ev1, ctx->stream);
+    ctx->timed = true;
+    ctx->launches += 1;
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "back substitution launch");
+    return 0;
+}
+
+// ---- host entry points -----------------------------------------------------------
+static int solve_host(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t m, int64_t n,
+                      const double* a, const double* b, double* q, double* r, double* x, double* z,
+                      xqr_status* st) {
+    if (!ctx) return XQR_USAGE;
+    if (int c = check_shape(ctx, st, limbs, batch, m, n)) {
+        for (int64_t s = 1; s < batch && st; ++s) fill_status(st + s, c, 0, s);
+        return c;
+    }
+    if (batch == 0) return 0;
+    cudaSetDevice(ctx->device);
+    const size_t L2 = 2 * (size_t)limbs;
+    const size_t a_b = sizeof(double) * batch * m * n * L2;
+    const size_t b_b = lsq ? sizeof(double) * batch * m * L2 : 0;
+    const size_t q_b = lsq ? 0 : a_b;
+    const size_t r_b = lsq ? 0 : sizeof(double) * batch * n * n * L2;
+    const size_t x_b = lsq ? sizeof(double) * batch * n * L2 : 0;
+    const size_t z_b = lsq ? sizeof(double) * batch * limbs : 0;
+    const size_t s_b = sizeof(xqr_status) * batch;
+    arena_plan plan;
+    size_t o_a = plan.add(a_b), o_b = plan.add(b_b), o_q = plan.add(q_b), o_r = plan.add(r_b),
+           o_x = plan.add(x_b), o_z = plan.add(z_b), o_s = plan.add(s_b);
+    // the solver scratch goes after the I/O regions; make sure the arena is
+    // large enough for the I/O regions before taking pointers into it
+    const int ncol = (int)n + (lsq ? 1 : 0);
+    size_t scratch = sizeof(double) * (size_t)batch *
+                     (xb::ws_doubles(limbs, (int)m, ncol) + (lsq ? xb::rws_doubles(limbs, (int)n) : 0));
+    cudaError_t e = ensure_arena(ctx, plan.total + scratch + 512);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
+    // stage inputs through pinned memory
+    e = ensure_pinned(ctx, a_b + b_b);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "pinned staging allocation");
+    char* pin = static_cast<char*>(ctx->pinned);
+    std::memcpy(pin, a, a_b);
+    if (lsq) std::memcpy(pin + a_b, b, b_b);
+    cudaMemcpyAsync(at(ctx, o_a), pin, a_b, cudaMemcpyHostToDevice, ctx->stream);
+    if (lsq) cudaMemcpyAsync(at(ctx, o_b), pin + a_b, b_b, cudaMemcpyHostToDevice, ctx->stream);
+    int rc = solve_device(ctx, lsq, limbs, batch, m, n, (const double*)at(ctx, o_a),
+                          (const double*)at(ctx, o_b), (double*)at(ctx, o_q), (double*)at(ctx, o_r),
+                          (double*)at(ctx, o_x), (double*)at(ctx, o_z),
+                          (xqr_status*)at(ctx, o_s), plan.total, true);
+    if (rc) return rc;
+    std::vector<xqr_status> hst(batch);
+    cudaMemcpyAsync(hst.data(), at(ctx, o_s), s_b, cudaMemcpyDeviceToHost, ctx->stream);
+    if (lsq) {
+        cudaMemcpyAsync(x, at(ctx, o_x), x_b, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(z, at(ctx, o_z), z_b, cudaMemcpyDeviceToHost, ctx->stream);
+    } else {
+        cudaMemcpyAsync(q, at(ctx, o_q), q_b, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(r, at(ctx, o_r), r_b, cudaMemcpyDeviceToHost, ctx->stream);
+    }
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "solve");
+    if (st) std::memcpy(st, hst.data(), s_b);
+    return first_code(hst);
+}
+
+int xqr_mgs_qr(xqr_ctx* ctx, int limbs, int64_t m, int64_t n, const double* a, double* q,
+               double* r, xqr_status* st) {
+    return solve_host(ctx, false, limbs, 1, m, n, a, nullptr, q, r, nullptr, nullptr, st);
+}
+
+int xqr_lsq_solve(xqr_ctx* ctx, int limbs, int64_t m, int64_t n, const double* a,
+                  const double* b, double* x, double* z, xqr_status* st) {
+    return solve_host(ctx, true, limbs, 1, m, n, a, b, nullptr, nullptr, x, z, st);
+}
+
+int xqr_mgs_qr_batched(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                       const double* a, double* q, double* r, xqr_status* st) {
+    return solve_host(ctx, false, limbs, batch, m, n, a, nullptr, q, r, nullptr, nullptr, st);
+}
+
+int xqr_lsq_solve_batched(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                          const double* a, const double* b, double* x, double* z,
+                          xqr_status* st) {
+    return solve_host(ctx, true, limbs, batch, m, n, a, b, nullptr, nullptr, x, z, st);
+}
+
+int xqr_back_substitute(xqr_ctx* ctx, int limbs, int64_t rows, int64_t cols, const double* r,
+                        int64_t ylen, const double* y, double* x, xqr_status* st) {
+    if (!ctx) return XQR_USAGE;
+    if (!valid_limbs(limbs)) return fail(ctx, st, XQR_USAGE, "limbs must be 1, 2 or 4");
+    // mgs.hpp:113-114
+    if (rows != cols) return fail(ctx, st, XQR_DIMENSION, "triangular factor must be square");
+    if (ylen != cols) return fail(ctx, st, XQR_DIMENSION, "right-hand side length mismatch");
+    if (cols < 1) return fail(ctx, st, XQR_DIMENSION, "empty triangular factor");
+    cudaSetDevice(ctx->device);
+    const int64_t n = cols;
+    const size_t L2 = 2 * (size_t)limbs;
+    const size_t r_b = sizeof(double) * n * n * L2, y_b = sizeof(double) * n * L2;
+    const size_t prep_b = sizeof(double) * n * (3 * limbs + 1);
+    arena_plan plan;
+    size_t o_p = plan.add(prep_b), o_r = plan.add(r_b), o_y = plan.add(y_b), o_x = plan.add(y_b),
+           o_s = plan.add(sizeof(xqr_status));
+    cudaError_t e = ensure_arena(ctx, plan.total + 256);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
+    cudaMemcpyAsync(at(ctx, o_r), r, r_b, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(at(ctx, o_y), y, y_b, cudaMemcpyHostToDevice, ctx->stream);
+    xb::BackSubParams p{1, (int)n, (const double*)at(ctx, o_r), (const double*)at(ctx, o_y),
+                        (double*)at(ctx, o_x), (xqr_status*)at(ctx, o_s), (double*)at(ctx, o_p)};
+    e = xb::launch_back_substitute(limbs, p, ctx->stream);
+    ctx->launches += 1;
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "back substitution launch");
+    xqr_status hs;
+    cudaMemcpyAsync(&hs, at(ctx, o_s), sizeof hs, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(x, at(ctx, o_x), y_b, cudaMemcpyDeviceToHost, ctx->stream);
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "back substitution");
+    if (st) *st = hs;
+    return hs.code;
+}
+
+int xqr_arith(xqr_ctx* ctx, int limbs, int op, int64_t count, const double* a, const double* b,
+              double* out, int32_t* codes) {
+    if (!ctx) return XQR_USAGE;
+    if (!valid_limbs(limbs) || op < 0 || op > 8) return XQR_USAGE;
+    cudaSetDevice(ctx->device);
+    const size_t stride = (op >= 5 && op <= 7) ? 2 * limbs : limbs;
+    const size_t bytes = sizeof(double) * stride * count;
+    arena_plan plan;
+    size_t o_a = plan.add(bytes), o_b = plan.add(bytes), o_o = plan.add(bytes),
+           o_c = plan.add(sizeof(int32_t) * count);
+    cudaError_t e = ensure_arena(ctx, plan.total + 256);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
+    cudaMemcpyAsync(at(ctx, o_a), a, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (b) cudaMemcpyAsync(at(ctx, o_b), b, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    e = xb::launch_arith(limbs, op, count, (const double*)at(ctx, o_a),
+                         b ? (const double*)at(ctx, o_b) : nullptr, (double*)at(ctx, o_o),
+                         (int32_t*)at(ctx, o_c), ctx->stream);
+    ctx->launches += 1;
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "arith launch");
+    cudaMemcpyAsync(out, at(ctx, o_o), bytes, cudaMemcpyDeviceToHost, ctx->stream);
+    if (codes) cudaMemcpyAsync(codes, at(ctx, o_c), sizeof(int32_t) * count, cudaMemcpyDeviceToHost,
+                               ctx->stream);
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "arith");
+    return 0;
+}
+
+}  // extern "C"

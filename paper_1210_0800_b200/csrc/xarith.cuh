@@ -1,0 +1,584 @@
+// xarith.cuh -- device-inline double / double-double / quad-double arithmetic.
+//
+// Each operation executes exactly the FP64 operations of the reference, in
+// the reference's order, on the same operands, so results are bit-identical:
+//   eft.hpp:24-72, double_double.hpp:41-122, quad_double.hpp:41-385.
+// Every DADD/DMUL/DFMA is an explicit __dadd_rn/__dmul_rn/__fma_rn so nvcc can
+// never contract a*b+c (the reference builds with -ffp-contract=off,
+// proj/CMakeLists.txt:15); the library is also compiled with --fmad=false.
+// Limbs live in registers; nothing here touches memory.
+//
+// Overflow: the reference throws overflow_error from every checked op whose
+// leading limb is not finite (double_double.hpp:34-37, quad_double.hpp:202-205).
+// The device instead lets Inf/NaN propagate (they are absorbing through
+// +,*, and the renormalisations keep a non-finite head) and the kernels test
+// the head limb of each finished column / coefficient -- see DESIGN.md §5.
+#pragma once
+#include <cstdint>
+
+namespace xb {
+
+#define XB_DEV __device__ __forceinline__
+
+XB_DEV double dadd(double a, double b) { return __dadd_rn(a, b); }
+XB_DEV double dsub(double a, double b) { return __dsub_rn(a, b); }
+XB_DEV double dmul(double a, double b) { return __dmul_rn(a, b); }
+XB_DEV double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// ---- error-free transforms (eft.hpp) --------------------------------------
+// eft.hpp:24-30
+XB_DEV void two_sum(double a, double b, double& s, double& e) {
+    s = dadd(a, b);
+    double bb = dsub(s, a);
+    double ea = dsub(a, dsub(s, bb));
+    double eb = dsub(b, bb);
+    e = dadd(ea, eb);
+}
+// eft.hpp:33-37
+XB_DEV void quick_two_sum(double a, double b, double& s, double& e) {
+    s = dadd(a, b);
+    e = dsub(b, dsub(s, a));
+}
+// eft.hpp:59-62 (the FMA path eft.hpp:66-72 selects on FMA hardware)
+XB_DEV void two_prod(double a, double b, double& p, double& e) {
+    p = dmul(a, b);
+    e = dfma(a, b, -p);
+}
+
+XB_DEV bool finite(double x) {
+    return (__double_as_longlong(x) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;
+}
+XB_DEV bool is_inf(double x) {
+    return (__double_as_longlong(x) & 0x7fffffffffffffffll) == 0x7ff0000000000000ll;
+}
+
+// ---- real types -------------------------------------------------------------
+struct r1 {  // double (real_type.hpp:16-20)
+    double c0;
+};
+struct r2 {  // double_double {hi, lo} (double_double.hpp:15-22)
+    double c0, c1;
+};
+struct r4 {  // quad_double c[4] (quad_double.hpp:19-26)
+    double c0, c1, c2, c3;
+};
+
+template <int L>
+struct real_of;
+template <>
+struct real_of<1> {
+    using type = r1;
+    static constexpr double eps = 0x1p-52;  // real_type.hpp:38
+};
+template <>
+struct real_of<2> {
+    using type = r2;
+    static constexpr double eps = 0x1p-104;  // real_type.hpp:43
+};
+template <>
+struct real_of<4> {
+    using type = r4;
+    static constexpr double eps = 0x1p-209;  // real_type.hpp:46
+};
+
+XB_DEV r1 make1(double v) { return {v}; }
+XB_DEV r2 make2(double v) { return {v, 0.0}; }
+XB_DEV r4 make4(double v) { return {v, 0.0, 0.0, 0.0}; }
+template <class R>
+XB_DEV R rmake(double v);
+template <>
+XB_DEV r1 rmake<r1>(double v) { return make1(v); }
+template <>
+XB_DEV r2 rmake<r2>(double v) { return make2(v); }
+template <>
+XB_DEV r4 rmake<r4>(double v) { return make4(v); }
+
+XB_DEV double head(const r1& a) { return a.c0; }
+XB_DEV double head(const r2& a) { return a.c0; }
+XB_DEV double head(const r4& a) { return a.c0; }
+
+// ---- double ---------------------------------------------------------------
+XB_DEV r1 add(const r1& a, const r1& b) { return {dadd(a.c0, b.c0)}; }
+XB_DEV r1 neg(const r1& a) { return {-a.c0}; }
+XB_DEV r1 sub(const r1& a, const r1& b) { return {dsub(a.c0, b.c0)}; }
+XB_DEV r1 mul(const r1& a, const r1& b) { return {dmul(a.c0, b.c0)}; }
+XB_DEV r1 rsqrt_ref(const r1& a) { return {__dsqrt_rn(a.c0)}; }
+XB_DEV r1 div(const r1& a, const r1& b) { return {__ddiv_rn(a.c0, b.c0)}; }
+XB_DEV bool lt(const r1& a, const r1& b) { return a.c0 < b.c0; }
+XB_DEV bool le(const r1& a, const r1& b) { return a.c0 <= b.c0; }
+XB_DEV bool ge(const r1& a, const r1& b) { return a.c0 >= b.c0; }
+XB_DEV bool is_zero(const r1& a) { return a.c0 == 0.0; }
+XB_DEV r1 rabs(const r1& a) { return {fabs(a.c0)}; }
+
+// ---- double_double (double_double.hpp) -------------------------------------
+// double_double.hpp:41-47
+XB_DEV r2 add(const r2& a, const r2& b) {
+    double s, se, t, te, v, ve, z, ze;
+    two_sum(a.c0, b.c0, s, se);
+    two_sum(a.c1, b.c1, t, te);
+    quick_two_sum(s, dadd(se, t), v, ve);
+    quick_two_sum(v, dadd(ve, te), z, ze);
+    return {z, ze};
+}
+XB_DEV r2 neg(const r2& a) { return {-a.c0, -a.c1}; }       // :49
+XB_DEV r2 sub(const r2& a, const r2& b) { return add(a, neg(b)); }  // :51-53
+// double_double.hpp:56-63
+XB_DEV r2 mul(const r2& a, const r2& b) {
+    double p, pe, z, ze;
+    two_prod(a.c0, b.c0, p, pe);
+    double t = dmul(a.c1, b.c1);
+    t = dfma(a.c0, b.c1, t);
+    t = dfma(a.c1, b.c0, t);
+    quick_two_sum(p, dadd(pe, t), z, ze);
+    return {z, ze};
+}
+// double_double.hpp:66-70
+XB_DEV r2 dd_add_d(const r2& a, double b) {
+    double s, se, z, ze;
+    two_sum(a.c0, b, s, se);
+    quick_two_sum(s, dadd(se, a.c1), z, ze);
+    return {z, ze};
+}
+// double_double.hpp:72-76
+XB_DEV r2 dd_mul_d(const r2& a, double b) {
+    double p, pe, z, ze;
+    two_prod(a.c0, b, p, pe);
+    quick_two_sum(p, dfma(a.c1, b, pe), z, ze);
+    return {z, ze};
+}
+// double_double.hpp:94-104 (a >= 0, non-zero checked by caller semantics)
+XB_DEV r2 rsqrt_ref(const r2& a) {
+    if (a.c0 == 0.0 && a.c1 == 0.0) return {0.0, 0.0};
+    double x = __ddiv_rn(1.0, __dsqrt_rn(a.c0));
+    double ax = dmul(a.c0, x);
+    double sq, sqe;
+    two_prod(ax, ax, sq, sqe);
+    r2 diff = sub(a, r2{sq, sqe});
+    double corr = dmul(diff.c0, dmul(x, 0.5));
+    double z, ze;
+    quick_two_sum(ax, corr, z, ze);
+    return {z, ze};
+}
+// double_double.hpp:106-115
+XB_DEV bool lt(const r2& a, const r2& b) { return a.c0 < b.c0 || (a.c0 == b.c0 && a.c1 < b.c1); }
+XB_DEV bool le(const r2& a, const r2& b) { return !lt(b, a); }
+XB_DEV bool ge(const r2& a, const r2& b) { return !lt(a, b); }
+XB_DEV bool is_zero(const r2& a) { return a.c0 == 0.0 && a.c1 == 0.0; }
+XB_DEV r2 rabs(const r2& a) { return a.c0 < 0.0 ? neg(a) : a; }  // :117
+
+// ---- quad_double (quad_double.hpp) -------------------------------------------
+// quad_double.hpp:41-48
+XB_DEV void three_sum(double& a, double& b, double& c) {
+    double t, te, u, ue, v, ve;
+    two_sum(a, b, t, te);
+    two_sum(c, t, u, ue);
+    two_sum(te, ue, v, ve);
+    a = u;
+    b = v;
+    c = ve;
+}
+// quad_double.hpp:60-75
+XB_DEV double quick_three_accum(double& a, double& b, double c) {
+    double t, te, u, ue;
+    two_sum(b, c, t, te);
+    two_sum(a, t, u, ue);
+    b = te;
+    a = ue;
+    bool za = (a != 0.0);
+    bool zb = (b != 0.0);
+    if (za && zb) return u;
+    if (!zb) {
+        b = a;
+        a = u;
+    } else {
+        a = u;
+    }
+    return 0.0;
+}
+// quad_double.hpp:78-154.  The three-level branch tree is written as a
+// pointer walk over (s0..s3): each level does one quick_two_sum at the
+// current slot p, and advances p when the error term is non-zero.  Same ops,
+// same operands, same order as every path of the reference tree.
+XB_DEV void renorm5(double& c0, double& c1, double& c2, double& c3, double c4) {
+    if (is_inf(c0)) return;
+    double t, e;
+    quick_two_sum(c3, c4, t, e);
+    c4 = e;
+    quick_two_sum(c2, t, t, e);
+    c3 = e;
+    quick_two_sum(c1, t, t, e);
+    c2 = e;
+    quick_two_sum(c0, t, t, e);
+    c1 = e;
+    c0 = t;
+
+    double s0 = c0, s1 = c1, s2 = 0.0, s3 = 0.0;
+    if (s1 != 0.0) {
+        quick_two_sum(s1, c2, s1, s2);
+        if (s2 != 0.0) {
+            quick_two_sum(s2, c3, s2, s3);
+            if (s3 != 0.0)
+                s3 = dadd(s3, c4);
+            else
+                s2 = dadd(s2, c4);
+        } else {
+            quick_two_sum(s1, c3, s1, s2);
+            if (s2 != 0.0)
+                quick_two_sum(s2, c4, s2, s3);
+            else
+                quick_two_sum(s1, c4, s1, s2);
+        }
+    } else {
+        quick_two_sum(s0, c2, s0, s1);
+        if (s1 != 0.0) {
+            quick_two_sum(s1, c3, s1, s2);
+            if (s2 != 0.0)
+                quick_two_sum(s2, c4, s2, s3);
+            else
+                quick_two_sum(s1, c4, s1, s2);
+        } else {
+            quick_two_sum(s0, c3, s0, s1);
+            if (s1 != 0.0)
+                quick_two_sum(s1, c4, s1, s2);
+            else
+                quick_two_sum(s0, c4, s0, s1);
+        }
+    }
+    c0 = s0;
+    c1 = s1;
+    c2 = s2;
+    c3 = s3;
+}
+// quad_double.hpp:157-200
+XB_DEV void renorm4(double& c0, double& c1, double& c2, double& c3) {
+    if (is_inf(c0)) return;
+    double t, e;
+    quick_two_sum(c2, c3, t, e);
+    c3 = e;
+    quick_two_sum(c1, t, t, e);
+    c2 = e;
+    quick_two_sum(c0, t, t, e);
+    c1 = e;
+    c0 = t;
+
+    double s0 = c0, s1 = c1, s2 = 0.0, s3 = 0.0;
+    if (s1 != 0.0) {
+        quick_two_sum(s1, c2, s1, s2);
+        if (s2 != 0.0)
+            quick_two_sum(s2, c3, s2, s3);
+        else
+            quick_two_sum(s1, c3, s1, s2);
+    } else {
+        quick_two_sum(s0, c2, s0, s1);
+        if (s1 != 0.0)
+            quick_two_sum(s1, c3, s1, s2);
+        else
+            quick_two_sum(s0, c3, s0, s1);
+    }
+    c0 = s0;
+    c1 = s1;
+    c2 = s2;
+    c3 = s3;
+}
+
+XB_DEV double pick4(int i, double x0, double x1, double x2, double x3) {
+    double r = x3;
+    r = (i == 2) ? x2 : r;
+    r = (i == 1) ? x1 : r;
+    r = (i == 0) ? x0 : r;
+    return r;
+}
+
+// quad_double.hpp:216-257: merge the eight limbs by decreasing magnitude of
+// the current heads, accumulate with quick_three_accum, fold the leftovers
+// into x[3] (a's first, then b's), renormalise.  Indices stay in registers;
+// limb reads are register selects, never local-memory indexing.
+XB_DEV r4 add(const r4& a, const r4& b) {
+    int i = 0, j = 0, k = 0;
+    double u, v;
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+
+    if (fabs(a.c0) > fabs(b.c0)) {
+        u = a.c0;
+        i = 1;
+    } else {
+        u = b.c0;
+        j = 1;
+    }
+    {
+        double ai = pick4(i, a.c0, a.c1, a.c2, a.c3);
+        double bj = pick4(j, b.c0, b.c1, b.c2, b.c3);
+        if (fabs(ai) > fabs(bj)) {
+            v = ai;
+            ++i;
+        } else {
+            v = bj;
+            ++j;
+        }
+    }
+    quick_two_sum(u, v, u, v);
+
+    while (k < 4) {
+        if (i >= 4 && j >= 4) {
+            // x[k] = u; if (k < 3) x[++k] = v;
+            x0 = (k == 0) ? u : x0;
+            x1 = (k == 1) ? u : x1;
+            x2 = (k == 2) ? u : x2;
+            x3 = (k == 3) ? u : x3;
+            x1 = (k == 0) ? v : x1;
+            x2 = (k == 1) ? v : x2;
+            x3 = (k == 2) ? v : x3;
+            break;
+        }
+        double ai = pick4(i, a.c0, a.c1, a.c2, a.c3);
+        double bj = pick4(j, b.c0, b.c1, b.c2, b.c3);
+        bool take_a = (j >= 4) || (i < 4 && fabs(ai) > fabs(bj));
+        double s = take_a ? ai : bj;
+        i += take_a ? 1 : 0;
+        j += take_a ? 0 : 1;
+        double d = quick_three_accum(u, v, s);
+        if (d != 0.0) {
+            x0 = (k == 0) ? d : x0;
+            x1 = (k == 1) ? d : x1;
+            x2 = (k == 2) ? d : x2;
+            x3 = (k == 3) ? d : x3;
+            ++k;
+        }
+    }
+    // for (; i < 4; ++i) x[3] += a.c[i]; for (; j < 4; ++j) x[3] += b.c[j];
+    if (i <= 0) x3 = dadd(x3, a.c0);
+    if (i <= 1) x3 = dadd(x3, a.c1);
+    if (i <= 2) x3 = dadd(x3, a.c2);
+    if (i <= 3) x3 = dadd(x3, a.c3);
+    if (j <= 0) x3 = dadd(x3, b.c0);
+    if (j <= 1) x3 = dadd(x3, b.c1);
+    if (j <= 2) x3 = dadd(x3, b.c2);
+    if (j <= 3) x3 = dadd(x3, b.c3);
+
+    renorm4(x0, x1, x2, x3);
+    return {x0, x1, x2, x3};
+}
+XB_DEV r4 neg(const r4& a) { return {-a.c0, -a.c1, -a.c2, -a.c3}; }  // :259-261
+// renormalize (real_type.hpp:20, double_double.hpp:28-31, quad_double.hpp:209-213)
+XB_DEV r1 renormalize(const r1& a) { return a; }
+XB_DEV r2 renormalize(const r2& a) {
+    r2 o;
+    quick_two_sum(a.c0, a.c1, o.c0, o.c1);
+    return o;
+}
+XB_DEV r4 renormalize(const r4& a) {
+    r4 o = a;
+    renorm4(o.c0, o.c1, o.c2, o.c3);
+    return o;
+}
+XB_DEV r4 sub(const r4& a, const r4& b) { return add(a, neg(b)); }     // :263
+
+// quad_double.hpp:267-338
+XB_DEV r4 mul(const r4& a, const r4& b) {
+    double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5;
+    two_prod(a.c0, b.c0, p0, q0);
+    two_prod(a.c0, b.c1, p1, q1);
+    two_prod(a.c1, b.c0, p2, q2);
+    two_prod(a.c0, b.c2, p3, q3);
+    two_prod(a.c1, b.c1, p4, q4);
+    two_prod(a.c2, b.c0, p5, q5);
+
+    three_sum(p1, p2, q0);
+
+    three_sum(p2, q1, q2);
+    three_sum(p3, p4, p5);
+    double s0, t0, s1, t1;
+    two_sum(p2, p3, s0, t0);
+    two_sum(q1, p4, s1, t1);
+    // (s2 = q2 + p5; s2 += t0 + t1 is dead in the reference: never read)
+    two_sum(s1, t0, s1, t0);
+
+    double p6, q6, p7, q7, p8, q8, p9, q9;
+    two_prod(a.c0, b.c3, p6, q6);
+    two_prod(a.c1, b.c2, p7, q7);
+    two_prod(a.c2, b.c1, p8, q8);
+    two_prod(a.c3, b.c0, p9, q9);
+
+    two_sum(q0, q3, q0, q3);
+    two_sum(q4, q5, q4, q5);
+    two_sum(p6, p7, p6, p7);
+    two_sum(p8, p9, p8, p9);
+
+    double t0b, t1b;
+    two_sum(q0, q4, t0b, t1b);
+    t1b = dadd(t1b, dadd(q3, q5));
+
+    double r0, r1;
+    two_sum(p6, p8, r0, r1);
+    r1 = dadd(r1, dadd(p7, p9));
+
+    double q3b, q4b;
+    two_sum(t0b, r0, q3b, q4b);
+    q4b = dadd(q4b, dadd(t1b, r1));
+
+    double t0c, t1c;
+    two_sum(q3b, s1, t0c, t1c);
+    t1c = dadd(t1c, q4b);
+
+    // t1c += a1*b3 + a2*b2 + a3*b1 + q6 + q7 + q8 + q9 (left to right)
+    double w = dadd(dmul(a.c1, b.c3), dmul(a.c2, b.c2));
+    w = dadd(w, dmul(a.c3, b.c1));
+    w = dadd(w, q6);
+    w = dadd(w, q7);
+    w = dadd(w, q8);
+    w = dadd(w, q9);
+    t1c = dadd(t1c, w);
+
+    renorm5(p0, p1, s0, t0c, t1c);
+    return {p0, p1, s0, t0c};
+}
+XB_DEV r4 mul_pwr2(const r4& a, double p2) {  // :341-343
+    return {dmul(a.c0, p2), dmul(a.c1, p2), dmul(a.c2, p2), dmul(a.c3, p2)};
+}
+// quad_double.hpp:359-370
+XB_DEV r4 rsqrt_ref(const r4& a) {
+    if (a.c0 == 0.0 && a.c1 == 0.0 && a.c2 == 0.0 && a.c3 == 0.0) return {0.0, 0.0, 0.0, 0.0};
+    r4 x = make4(__ddiv_rn(1.0, __dsqrt_rn(a.c0)));
+#pragma unroll 1
+    for (int it = 0; it < 2; ++it) {
+        r4 t = mul(a, x);
+        x = add(x, mul_pwr2(mul(x, sub(make4(1.0), mul(t, x))), 0.5));
+    }
+    r4 y = mul(a, x);
+    y = add(y, mul_pwr2(mul(sub(a, mul(y, y)), x), 0.5));
+    return y;
+}
+// quad_double.hpp:372-383
+XB_DEV bool lt(const r4& a, const r4& b) {
+    if (a.c0 < b.c0) return true;
+    if (a.c0 > b.c0) return false;
+    if (a.c1 < b.c1) return true;
+    if (a.c1 > b.c1) return false;
+    if (a.c2 < b.c2) return true;
+    if (a.c2 > b.c2) return false;
+    return a.c3 < b.c3;
+}
+XB_DEV bool le(const r4& a, const r4& b) { return !lt(b, a); }
+XB_DEV bool ge(const r4& a, const r4& b) { return !lt(a, b); }
+XB_DEV bool is_zero(const r4& a) { return a.c0 == 0.0 && a.c1 == 0.0 && a.c2 == 0.0 && a.c3 == 0.0; }
+XB_DEV r4 rabs(const r4& a) { return a.c0 < 0.0 ? neg(a) : a; }  // :385
+
+// ---- division with the divisor-only part hoisted -------------------------------
+// The reference division (double_double.hpp:80-90, quad_double.hpp:346-355)
+// first builds a reciprocal estimate from the divisor alone, then runs a
+// short tail on the dividend.  recip() is that divisor-only prefix; divide()
+// is the tail.  divide(a, b, recip(b)) == a / b bit for bit, so a pivot
+// computes recip(r_kk) once and every row reuses it.
+// Status from recip(): 0 ok, 3 = domain (b == 0), 2 = overflow (1/b not finite).
+template <class R>
+struct recip_t;
+template <>
+struct recip_t<r1> {
+    double b;
+};
+template <>
+struct recip_t<r2> {
+    r2 x1;
+};
+template <>
+struct recip_t<r4> {
+    r4 x;
+};
+
+// plain IEEE division for double (real_type.hpp: no checked funnel)
+XB_DEV recip_t<r1> recip(const r1& b, int& status) { return {b.c0}; }
+XB_DEV r1 div_plain(const r1& a, const r1& b) { return {__ddiv_rn(a.c0, b.c0)}; }
+XB_DEV r1 divide(const r1& a, const r1& b, const recip_t<r1>& rc) { return {__ddiv_rn(a.c0, rc.b)}; }
+
+XB_DEV recip_t<r2> recip(const r2& b, int& status) {
+    if (b.c0 == 0.0) {
+        status = 3;
+        return {{0.0, 0.0}};
+    }
+    double x0 = __ddiv_rn(1.0, b.c0);
+    if (!finite(x0)) status = 2;
+    r2 e = sub(make2(1.0), dd_mul_d(b, x0));
+    return {dd_add_d(dd_mul_d(e, x0), x0)};
+}
+XB_DEV r2 divide(const r2& a, const r2& b, const recip_t<r2>& rc) {
+    r2 q = mul(a, rc.x1);
+    r2 r = sub(a, mul(b, q));
+    return add(q, mul(r, rc.x1));
+}
+
+XB_DEV recip_t<r4> recip(const r4& b, int& status) {
+    if (b.c0 == 0.0) {
+        status = 3;
+        return {{0.0, 0.0, 0.0, 0.0}};
+    }
+    double seed = __ddiv_rn(1.0, b.c0);
+    if (!finite(seed)) status = 2;
+    r4 x = make4(seed);
+#pragma unroll 1
+    for (int it = 0; it < 2; ++it) x = add(x, mul(x, sub(make4(1.0), mul(b, x))));
+    return {x};
+}
+XB_DEV r4 divide(const r4& a, const r4& b, const recip_t<r4>& rc) {
+    r4 q = mul(a, rc.x);
+    return add(q, mul(rc.x, sub(a, mul(b, q))));
+}
+
+template <class R>
+XB_DEV R rdiv(const R& a, const R& b, int& status) {
+    recip_t<R> rc = recip(b, status);
+    return divide(a, b, rc);
+}
+
+// ---- complex (complex.hpp) -------------------------------------------------------
+template <class R>
+struct cx {
+    R re, im;
+};
+
+template <class R>
+XB_DEV cx<R> cconj(const cx<R>& z) {  // complex.hpp:21-24
+    return {z.re, neg(z.im)};
+}
+template <class R>
+XB_DEV cx<R> cadd(const cx<R>& a, const cx<R>& b) {  // :26-29
+    return {add(a.re, b.re), add(a.im, b.im)};
+}
+template <class R>
+XB_DEV cx<R> csub(const cx<R>& a, const cx<R>& b) {  // :31-34
+    return {sub(a.re, b.re), sub(a.im, b.im)};
+}
+template <class R>
+XB_DEV cx<R> cmul(const cx<R>& a, const cx<R>& b) {  // :41-44
+    return {sub(mul(a.re, b.re), mul(a.im, b.im)), add(mul(a.re, b.im), mul(a.im, b.re))};
+}
+// Re(conj(a) * b): the real half of cmul(cconj(a), b), same ops.
+template <class R>
+XB_DEV R cdot_re(const cx<R>& a, const cx<R>& b) {
+    return sub(mul(a.re, b.re), mul(neg(a.im), b.im));
+}
+
+// Smith division (complex.hpp:47-58); status 3 on a zero divisor.
+template <class R>
+XB_DEV cx<R> cdiv(const cx<R>& a, const cx<R>& b, int& status) {
+    if (is_zero(b.re) && is_zero(b.im)) {
+        status = 3;
+        return a;
+    }
+    if (ge(rabs(b.re), rabs(b.im))) {
+        R t = rdiv(b.im, b.re, status);
+        R d = add(b.re, mul(b.im, t));
+        recip_t<R> rc = recip(d, status);
+        return {divide(add(a.re, mul(a.im, t)), d, rc), divide(sub(a.im, mul(a.re, t)), d, rc)};
+    }
+    R t = rdiv(b.re, b.im, status);
+    R d = add(mul(b.re, t), b.im);
+    recip_t<R> rc = recip(d, status);
+    return {divide(add(mul(a.re, t), a.im), d, rc), divide(sub(mul(a.im, t), a.re), d, rc)};
+}
+
+template <class R>
+XB_DEV bool cfinite(const cx<R>& z) {
+    return finite(head(z.re)) && finite(head(z.im));
+}
+
+}  // namespace xb

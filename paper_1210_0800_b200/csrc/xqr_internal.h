@@ -1,0 +1,73 @@
+// xqr_internal.h -- launch interface between the C ABI (capi.cu) and the
+// kernels (mgs_cta.cu, arith.cu).  Not part of the public boundary.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/xqr_b200.h"
+
+namespace xb {
+
+// Status key: the first error in the reference's program order wins
+// (atomicMin).  pos enumerates program points:
+//   0                      norm pre-pass (mgs.hpp:91-96 / :143)
+//   1 + k*(C+1)            normalize column k       (mgs.hpp:99 / :149)
+//   1 + k*(C+1) + (j-k)    remove_projection(k, j)   (mgs.hpp:101-103 / :150-153)
+//   1 + n*(C+1)            z = column_norm(b)        (mgs.hpp:155)
+//   2 + n*(C+1) + (n-1-k)  back substitution step k  (mgs.hpp:117-124)
+// with C = number of factored columns (n for QR, n+1 for LS).
+__host__ __device__ inline unsigned long long status_key(long long pos, int column, int code) {
+    return ((unsigned long long)pos << 24) | ((unsigned long long)(column & 0xFFFFF) << 4) |
+           (unsigned long long)code;
+}
+constexpr unsigned long long kNoError = ~0ull;
+
+struct SolveParams {
+    int64_t batch;
+    int m, n;
+    const double* a;  // AoS, batch * m*n*2L
+    const double* b;  // AoS, batch * m*2L (LS only)
+    double* q;        // AoS out (QR only)
+    double* r;        // AoS out n x n (QR only)
+    double* x;        // AoS out n (LS only)
+    double* z;        // L doubles per system (LS only)
+    xqr_status* st;   // per system
+    double* ws;       // lane-interleaved planar columns, ws_stride doubles per system
+    int64_t ws_stride;
+    double* rws;      // LS: R (n*n*2L) + y (n*2L) + Smith prep (n*(3L+1)) per system
+    int64_t rws_stride;
+};
+
+// rows-per-lane for a one-warp-per-column task
+inline int rows_per_lane(int m) {
+    int r = 1;
+    while (32 * r < m) r <<= 1;
+    return r;
+}
+constexpr int kMaxRowsPerLane = 32;  // m <= 1024
+
+// doubles of planar workspace per system
+inline int64_t ws_doubles(int limbs, int m, int ncols) {
+    return (int64_t)ncols * 2 * limbs * 32 * rows_per_lane(m);
+}
+inline int64_t rws_doubles(int limbs, int n) {
+    return (int64_t)n * n * 2 * limbs + (int64_t)n * 2 * limbs + (int64_t)n * (3 * limbs + 1);
+}
+
+cudaError_t launch_mgs_cta(int limbs, bool lsq, const SolveParams& p, cudaStream_t s);
+
+struct BackSubParams {
+    int64_t batch;
+    int n;
+    const double* r;  // AoS n x n per system
+    const double* y;  // AoS n per system
+    double* x;        // AoS n per system
+    xqr_status* st;
+    double* prep;     // n*(3L+1) per system
+};
+cudaError_t launch_back_substitute(int limbs, const BackSubParams& p, cudaStream_t s);
+
+cudaError_t launch_arith(int limbs, int op, int64_t count, const double* a, const double* b,
+                         double* out, int32_t* codes, cudaStream_t s);
+
+}  // namespace xb
