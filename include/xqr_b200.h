@@ -103,6 +103,16 @@ int xqr_back_substitute_batched_device(xqr_ctx* ctx, int limbs, int64_t batch, i
                                        const double* d_r, const double* d_y, double* d_x,
                                        xqr_status* d_st);
 
+/* ---- synthetic inputs (host) --------------------------------------------- */
+/* The reference generator: split_mix64 (random.hpp:17-41), log-uniform
+ * modulus in [10^-g, 10^g] computed in double and widened exactly
+ * (random.hpp:46-71), A column-major then b (experiment.hpp:64-79).
+ * first_stream < 0: one system from split_mix64(seed) itself (batch must be
+ * 1); else system s draws from split_mix64(seed).split(first_stream + s).
+ * b may be NULL.  Bitwise identical to the reference's draws. */
+int xqr_gen_systems(int limbs, int64_t batch, int64_t m, int64_t n, double g, uint64_t seed,
+                    int64_t first_stream, int threads, double* a, double* b);
+
 /* ---- test / instrumentation --------------------------------------------- */
 /* Elementwise device arithmetic, op codes as oracle/xqr_oracle.h xo_arith:
  * 0 add, 1 sub, 2 mul, 3 div, 4 sqrt, 5 cmul, 6 cdiv (Smith), 7 cadd,

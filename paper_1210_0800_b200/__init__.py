@@ -146,6 +146,8 @@ _SIGNATURES = {
     "xqr_lsq_solve_batched_device": ([_vp, _ci, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp], _ci),
     "xqr_back_substitute_batched_device": ([_vp, _ci, _i64, _i64, _vp, _vp, _vp, _vp], _ci),
     "xqr_arith": ([_vp, _ci, _ci, _i64, _dp, _dp, _dp, ctypes.POINTER(ctypes.c_int32)], _ci),
+    "xqr_gen_systems": ([_ci, _i64, _i64, _i64, ctypes.c_double, ctypes.c_uint64, _i64, _ci, _dp,
+                         _dp], _ci),
     "xqr_ctx_launch_count": ([_vp], _i64),
     "xqr_ctx_last_kernel_ms": ([_vp], ctypes.c_float),
 }
@@ -374,6 +376,23 @@ def mgs_qr_batched(a, device: int = 0, raise_first: bool = False):
         i = int(np.nonzero(codes)[0][0]) if codes.any() else 0
         _raise(rc, int(cols[i]) if batch else 0, ctx.last_error())
     return q, r, codes, cols
+
+
+def gen_systems(limbs: int, batch: int, m: int, n: int, g: float = 1.0, seed: int = 1,
+                first_stream: int = 0, threads: int | None = None, rhs: bool = True):
+    """The reference generator (experiment.hpp:64-79) on the host: returns
+    a (batch, n, m, 2, L) and b (batch, m, 2, L).  first_stream=-1 draws one
+    system from split_mix64(seed) itself (the reference's single-system
+    experiments); otherwise system s uses split_mix64(seed).split(first_stream+s)."""
+    lib = load_library()
+    a = np.zeros((batch, n, m, 2, limbs))
+    b = np.zeros((batch, m, 2, limbs)) if rhs else None
+    threads = threads or min(32, os.cpu_count() or 1)
+    rc = lib.xqr_gen_systems(limbs, batch, m, n, g, seed, first_stream, threads,
+                             a.ctypes.data_as(_dp), b.ctypes.data_as(_dp) if rhs else None)
+    if rc:
+        _raise(rc, what="gen_systems")
+    return (a, b) if rhs else a
 
 
 def arith(limbs: int, op: int, a, b=None, device: int = 0):

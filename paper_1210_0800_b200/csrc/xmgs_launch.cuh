@@ -1,0 +1,41 @@
+// xmgs_launch.cuh -- launch templates for the CTA-per-system MGS kernels.
+// Each (limbs, mode) pair is instantiated in its own translation unit
+// (mgs_L*_*.cu) so the heavy quad-double kernels compile in parallel.
+#pragma once
+#include "xmgs.cuh"
+
+namespace xb {
+
+constexpr int kWarps = 4;
+
+// Minimum resident CTAs per SM requested from ptxas (caps registers).
+template <int L, int LV>
+constexpr int min_blocks() {
+    return L == 4 ? (LV <= 3 ? 3 : 1) : (LV <= 3 ? 4 : 2);
+}
+
+template <int L, int LV, bool LSQ>
+static cudaError_t launch_one(const SolveParams& p, int rpl, cudaStream_t s) {
+    auto kern = mgs_cta_kernel<L, LV, kWarps, LSQ, min_blocks<L, LV>()>;
+    const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 32 * rpl);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<(unsigned)p.batch, kWarps * 32, smem, s>>>(p, rpl);
+    return cudaGetLastError();
+}
+
+// Stack depth 3 serves m <= 128 (the batched hot path) with the fewest
+// registers; depth 6 serves m <= 1024.
+template <int L, bool LSQ>
+static cudaError_t launch_rpl(const SolveParams& p, cudaStream_t s) {
+    const int rpl = rows_per_lane(p.m);
+    if (rpl <= 4) return launch_one<L, 3, LSQ>(p, rpl, s);
+    if (rpl <= kMaxRowsPerLane) return launch_one<L, 6, LSQ>(p, rpl, s);
+    return cudaErrorInvalidValue;
+}
+
+
+}  // namespace xb

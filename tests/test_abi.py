@@ -57,6 +57,7 @@ def test_cpp_dropin_headers_compile():
     src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
     with tempfile.TemporaryDirectory() as d:
         r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
+                            "-I", os.path.join(ROOT, "oracle"),
                             src], capture_output=True, text=True, cwd=d)
         assert r.returncode == 0, r.stderr
 
