@@ -232,7 +232,10 @@ def main():
     first = rank * per_rank
 
     ctx = xqr.Context(local)
-    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    # one explicit stream shared by torch (events, copies) and the C ABI
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
     a, b = xqr.gen_systems(limbs, per_rank, m, n, 1.0, 1, first)
     da = torch.from_numpy(a).cuda()
     db = torch.from_numpy(b).cuda()

@@ -4,7 +4,9 @@
 // device every entry point returns XQR_CUDA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -24,6 +26,8 @@ struct xqr_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timed = false;
     int64_t launches = 0;
+    int num_sms = 148;
+    bool coop = false;
     std::string last_error;
 };
 
@@ -109,11 +113,67 @@ int check_shape(xqr_ctx* ctx, xqr_status* st, int limbs, int64_t batch, int64_t 
     return 0;
 }
 
+// A single system large enough to feed several SMs goes to the persistent
+// grid kernel (xgrid.cuh); small ones stay on one CTA (xmgs.cuh).
+bool use_grid_path(xqr_ctx* ctx, int m, int n) {
+    if (const char* e = std::getenv("XQR_FORCE_CTA")) {
+        if (e[0] == '1') return false;
+    }
+    return ctx->coop && n >= 8 && m <= 256 * xb::kGridRowsPerThreadMax;
+}
+
+int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_a,
+               const double* d_b, double* d_q, double* d_r, double* d_x, double* d_z,
+               xqr_status* d_st, size_t scratch_off, bool timed) {
+    const int ncol = n + (lsq ? 1 : 0);
+    xb::GridParams p{};
+    p.m = m;
+    p.n = n;
+    p.rpt = xb::rows_per_thread(m);
+    p.a = d_a;
+    p.b = d_b;
+    p.q = d_q;
+    p.r = d_r;
+    p.x = d_x;
+    p.z = d_z;
+    p.st = d_st;
+    arena_plan plan;
+    const size_t o_ws = plan.add(sizeof(double) * (size_t)ncol * 2 * limbs * 256 * p.rpt);
+    const size_t o_rws = plan.add(lsq ? sizeof(double) * xb::rws_doubles(limbs, n) : 0);
+    const size_t o_nrm = plan.add(sizeof(double) * (size_t)ncol * limbs);
+    const size_t o_flg = plan.add(sizeof(int) * (size_t)n);
+    const size_t o_key = plan.add(sizeof(unsigned long long));
+    cudaError_t e = ensure_arena(ctx, scratch_off + plan.total + 256);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
+    p.ws = reinterpret_cast<double*>(at(ctx, scratch_off + o_ws));
+    p.rws = lsq ? reinterpret_cast<double*>(at(ctx, scratch_off + o_rws)) : nullptr;
+    p.norms = reinterpret_cast<double*>(at(ctx, scratch_off + o_nrm));
+    p.flags = reinterpret_cast<int*>(at(ctx, scratch_off + o_flg));
+    p.key = reinterpret_cast<unsigned long long*>(at(ctx, scratch_off + o_key));
+    cudaMemsetAsync(p.flags, 0, sizeof(int) * (size_t)n, ctx->stream);
+    cudaMemsetAsync(p.key, 0xFF, sizeof(unsigned long long), ctx->stream);
+    const int grid = std::min(ncol, ctx->num_sms);
+    if (timed) cudaEventRecord(ctx->ev0, ctx->stream);
+    switch (limbs) {
+        case 1: e = xb::launch_grid_L1(p, grid, lsq, ctx->stream); break;
+        case 2: e = xb::launch_grid_L2(p, grid, lsq, ctx->stream); break;
+        default: e = xb::launch_grid_L4(p, grid, lsq, ctx->stream); break;
+    }
+    if (timed) cudaEventRecord(ctx->ev1, ctx->stream);
+    ctx->timed = timed;
+    ctx->launches += 1;
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "grid kernel launch");
+    return 0;
+}
+
 // Device-side solve on device pointers (shared by host and device entry points).
 int solve_device(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t m, int64_t n,
                  const double* d_a, const double* d_b, double* d_q, double* d_r, double* d_x,
                  double* d_z, xqr_status* d_st, size_t scratch_off, bool timed) {
     const int ncol = (int)n + (lsq ? 1 : 0);
+    if (batch == 1 && use_grid_path(ctx, (int)m, (int)n))
+        return solve_grid(ctx, lsq, limbs, (int)m, (int)n, d_a, d_b, d_q, d_r, d_x, d_z, d_st,
+                          scratch_off, timed);
     xb::SolveParams p{};
     p.batch = batch;
     p.m = (int)m;
@@ -168,6 +228,11 @@ int xqr_ctx_create(int device, xqr_ctx** out) {
         return XQR_CUDA;
     }
     ctx->own_stream = true;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) == cudaSuccess) ctx->num_sms = v;
+    v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, device);
+    ctx->coop = v != 0;
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
     *out = ctx;
@@ -282,6 +347,11 @@ static int solve_host(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t 
     const int ncol = (int)n + (lsq ? 1 : 0);
     size_t scratch = sizeof(double) * (size_t)batch *
                      (xb::ws_doubles(limbs, (int)m, ncol) + (lsq ? xb::rws_doubles(limbs, (int)n) : 0));
+    if (batch == 1)  // grid path: rows padded to 256*rpt, plus norms / flags / key
+        scratch = std::max(scratch, sizeof(double) * ((size_t)ncol * 2 * limbs * 256 *
+                                                          xb::rows_per_thread((int)m) +
+                                                      (lsq ? xb::rws_doubles(limbs, (int)n) : 0) +
+                                                      (size_t)ncol * limbs + n) + 4096);
     cudaError_t e = ensure_arena(ctx, plan.total + scratch + 512);
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
     // stage inputs through pinned memory

@@ -1,0 +1,8 @@
+// mgs_grid_L2.cu -- instantiation unit for the single-system grid kernel (xgrid.cuh).
+#include "xgrid.cuh"
+
+namespace xb {
+cudaError_t launch_grid_L2(const GridParams& p, int grid, bool lsq, cudaStream_t s) {
+    return lsq ? launch_grid<2, true>(p, grid, s) : launch_grid<2, false>(p, grid, s);
+}
+}  // namespace xb

@@ -67,6 +67,34 @@ struct BackSubParams {
 };
 cudaError_t launch_back_substitute(int limbs, const BackSubParams& p, cudaStream_t s);
 
+// Single-system grid kernel (xgrid.cuh): one persistent cooperative CTA per SM.
+struct GridParams {
+    int m, n;
+    int rpt;            // rows per thread (power of two)
+    const double* a;    // AoS m x n
+    const double* b;    // AoS m (LS)
+    double* q;          // AoS out (QR)
+    double* r;          // AoS out n x n (QR)
+    double* x;          // AoS out n (LS)
+    double* z;          // L doubles (LS)
+    xqr_status* st;
+    double* ws;         // planar columns, ncol * COL doubles
+    double* rws;        // LS: R (n*n*2L) + y (n*2L) + Smith prep (n*(3L+1))
+    double* norms;      // ncol * L
+    int* flags;         // n: 0 pending, 1 published, 2 abort
+    unsigned long long* key;  // global status key (init kNoError)
+};
+
+constexpr int kGridRowsPerThreadMax = 4;  // m <= 1024
+inline int rows_per_thread(int m) {
+    int r = 1;
+    while (256 * r < m) r <<= 1;
+    return r;
+}
+cudaError_t launch_grid_L1(const GridParams& p, int grid, bool lsq, cudaStream_t s);
+cudaError_t launch_grid_L2(const GridParams& p, int grid, bool lsq, cudaStream_t s);
+cudaError_t launch_grid_L4(const GridParams& p, int grid, bool lsq, cudaStream_t s);
+
 cudaError_t launch_arith(int limbs, int op, int64_t count, const double* a, const double* b,
                          double* out, int32_t* codes, cudaStream_t s);
 
