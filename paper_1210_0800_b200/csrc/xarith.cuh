@@ -13,17 +13,49 @@
 // The device instead lets Inf/NaN propagate (they are absorbing through
 // +,*, and the renormalisations keep a non-finite head) and the kernels test
 // the head limb of each finished column / coefficient -- see DESIGN.md §5.
+//
+// The header also compiles as plain host C++ (g++ -ffp-contract=off): the
+// CPU test suite builds the very same arithmetic source into a host library
+// (tests/cpp/arith_host.cpp) and checks it bit for bit against the oracle.
 #pragma once
+#include <cmath>
 #include <cstdint>
+#include <cstring>
 
 namespace xb {
 
-#define XB_DEV __device__ __forceinline__
+#ifdef __CUDACC__
+#define XB_DEV __host__ __device__ __forceinline__
+#define XB_NOINLINE __host__ __device__ __noinline__
+#define XB_DEVICE __device__ __forceinline__  // device-only helpers (shuffles, ...)
+#else
+#define XB_DEV inline
+#define XB_NOINLINE
+#endif
 
+#ifdef __CUDA_ARCH__
 XB_DEV double dadd(double a, double b) { return __dadd_rn(a, b); }
 XB_DEV double dsub(double a, double b) { return __dsub_rn(a, b); }
 XB_DEV double dmul(double a, double b) { return __dmul_rn(a, b); }
 XB_DEV double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+XB_DEV double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+XB_DEV double dsqrt(double a) { return __dsqrt_rn(a); }
+XB_DEV long long dbits(double x) { return __double_as_longlong(x); }
+XB_DEV double dabs(double x) { return fabs(x); }
+#else
+XB_DEV double dadd(double a, double b) { return a + b; }
+XB_DEV double dsub(double a, double b) { return a - b; }
+XB_DEV double dmul(double a, double b) { return a * b; }
+XB_DEV double dfma(double a, double b, double c) { return std::fma(a, b, c); }
+XB_DEV double ddiv(double a, double b) { return a / b; }
+XB_DEV double dsqrt(double a) { return std::sqrt(a); }
+XB_DEV long long dbits(double x) {
+    long long v;
+    std::memcpy(&v, &x, sizeof v);
+    return v;
+}
+XB_DEV double dabs(double x) { return std::fabs(x); }
+#endif
 
 // ---- error-free transforms (eft.hpp) --------------------------------------
 // eft.hpp:24-30
@@ -46,10 +78,10 @@ XB_DEV void two_prod(double a, double b, double& p, double& e) {
 }
 
 XB_DEV bool finite(double x) {
-    return (__double_as_longlong(x) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;
+    return (dbits(x) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;
 }
 XB_DEV bool is_inf(double x) {
-    return (__double_as_longlong(x) & 0x7fffffffffffffffll) == 0x7ff0000000000000ll;
+    return (dbits(x) & 0x7fffffffffffffffll) == 0x7ff0000000000000ll;
 }
 
 // ---- real types -------------------------------------------------------------
@@ -102,13 +134,13 @@ XB_DEV r1 add(const r1& a, const r1& b) { return {dadd(a.c0, b.c0)}; }
 XB_DEV r1 neg(const r1& a) { return {-a.c0}; }
 XB_DEV r1 sub(const r1& a, const r1& b) { return {dsub(a.c0, b.c0)}; }
 XB_DEV r1 mul(const r1& a, const r1& b) { return {dmul(a.c0, b.c0)}; }
-XB_DEV r1 rsqrt_ref(const r1& a) { return {__dsqrt_rn(a.c0)}; }
-XB_DEV r1 div(const r1& a, const r1& b) { return {__ddiv_rn(a.c0, b.c0)}; }
+XB_DEV r1 rsqrt_ref(const r1& a) { return {dsqrt(a.c0)}; }
+XB_DEV r1 div(const r1& a, const r1& b) { return {ddiv(a.c0, b.c0)}; }
 XB_DEV bool lt(const r1& a, const r1& b) { return a.c0 < b.c0; }
 XB_DEV bool le(const r1& a, const r1& b) { return a.c0 <= b.c0; }
 XB_DEV bool ge(const r1& a, const r1& b) { return a.c0 >= b.c0; }
 XB_DEV bool is_zero(const r1& a) { return a.c0 == 0.0; }
-XB_DEV r1 rabs(const r1& a) { return {fabs(a.c0)}; }
+XB_DEV r1 rabs(const r1& a) { return {dabs(a.c0)}; }
 
 // ---- double_double (double_double.hpp) -------------------------------------
 // double_double.hpp:41-47
@@ -149,7 +181,7 @@ XB_DEV r2 dd_mul_d(const r2& a, double b) {
 // double_double.hpp:94-104 (a >= 0, non-zero checked by caller semantics)
 XB_DEV r2 rsqrt_ref(const r2& a) {
     if (a.c0 == 0.0 && a.c1 == 0.0) return {0.0, 0.0};
-    double x = __ddiv_rn(1.0, __dsqrt_rn(a.c0));
+    double x = ddiv(1.0, dsqrt(a.c0));
     double ax = dmul(a.c0, x);
     double sq, sqe;
     two_prod(ax, ax, sq, sqe);
@@ -292,13 +324,20 @@ XB_DEV double pick4(int i, double x0, double x1, double x2, double x3) {
 // quad_double.hpp:216-257: merge the eight limbs by decreasing magnitude of
 // the current heads, accumulate with quick_three_accum, fold the leftovers
 // into x[3] (a's first, then b's), renormalise.  Indices stay in registers;
-// limb reads are register selects, never local-memory indexing.
-XB_DEV r4 add(const r4& a, const r4& b) {
+// limb reads are register selects, never local-memory indexing.  This is the
+// general form; add() below runs it only for the lanes its fast path cannot
+// take.
+#ifdef XB_GENERAL_NOINLINE
+XB_NOINLINE
+#else
+XB_DEV
+#endif
+r4 add_general(const r4& a, const r4& b) {
     int i = 0, j = 0, k = 0;
     double u, v;
     double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
 
-    if (fabs(a.c0) > fabs(b.c0)) {
+    if (dabs(a.c0) > dabs(b.c0)) {
         u = a.c0;
         i = 1;
     } else {
@@ -308,7 +347,7 @@ XB_DEV r4 add(const r4& a, const r4& b) {
     {
         double ai = pick4(i, a.c0, a.c1, a.c2, a.c3);
         double bj = pick4(j, b.c0, b.c1, b.c2, b.c3);
-        if (fabs(ai) > fabs(bj)) {
+        if (dabs(ai) > dabs(bj)) {
             v = ai;
             ++i;
         } else {
@@ -332,7 +371,7 @@ XB_DEV r4 add(const r4& a, const r4& b) {
         }
         double ai = pick4(i, a.c0, a.c1, a.c2, a.c3);
         double bj = pick4(j, b.c0, b.c1, b.c2, b.c3);
-        bool take_a = (j >= 4) || (i < 4 && fabs(ai) > fabs(bj));
+        bool take_a = (j >= 4) || (i < 4 && dabs(ai) > dabs(bj));
         double s = take_a ? ai : bj;
         i += take_a ? 1 : 0;
         j += take_a ? 0 : 1;
@@ -356,6 +395,98 @@ XB_DEV r4 add(const r4& a, const r4& b) {
     if (j <= 3) x3 = dadd(x3, b.c3);
 
     renorm4(x0, x1, x2, x3);
+    return {x0, x1, x2, x3};
+}
+
+// One step of the reference merge loop on the next merged limb s:
+// quick_three_accum(u, v, s) (quad_double.hpp:60-75) and, when it returns a
+// non-zero component, x[k++] = it.  Branch-free: the zero tests become
+// selects, the indexed store a predicated write.  KMAX = the largest k this
+// step can see (k <= step index), so impossible slots cost nothing.
+template <int KMAX>
+XB_DEV void qadd_step(double& u, double& v, double s, int& k, double& x0, double& x1, double& x2,
+                      double& x3) {
+    double t, te, uu, ue;
+    two_sum(v, s, t, te);
+    two_sum(u, t, uu, ue);
+    const bool zb = (te != 0.0);
+    const bool emit = (ue != 0.0) && zb;
+    v = zb ? te : ue;
+    u = emit ? ue : uu;
+    x0 = (emit && k == 0) ? uu : x0;
+    if (KMAX >= 1) x1 = (emit && k == 1) ? uu : x1;
+    if (KMAX >= 2) x2 = (emit && k == 2) ? uu : x2;
+    if (KMAX >= 3) x3 = (emit && k == 3) ? uu : x3;
+    k += emit ? 1 : 0;
+}
+
+// renorm4 (quad_double.hpp:157-200) for the common case -- no infinity, no
+// zero error term along the way -- as straight-line code; any other lane
+// runs the reference branch tree.
+XB_DEV void renorm4_fast(double& c0, double& c1, double& c2, double& c3) {
+    double t, e, s0, s1, s2, s3, t1, e1;
+    quick_two_sum(c2, c3, t, e);
+    s3 = e;
+    quick_two_sum(c1, t, t, e);
+    s2 = e;
+    quick_two_sum(c0, t, s0, s1);
+    // s1 != 0 -> quick_two_sum(s1, c2'); s2' != 0 -> quick_two_sum(s2', c3')
+    quick_two_sum(s1, s2, t1, e1);
+    double u2, u3;
+    quick_two_sum(e1, s3, u2, u3);
+    if (!is_inf(c0) && s1 != 0.0 && e1 != 0.0) {
+        c0 = s0;
+        c1 = t1;
+        c2 = u2;
+        c3 = u3;
+    } else {
+        renorm4(c0, c1, c2, c3);
+    }
+}
+
+// quad_double.hpp:216-257, the same operations on the same operands in the
+// same order -- restructured for SIMT lanes that diverge on data.
+//
+// Fast path (no data-dependent branches).  When the limbs of a and b merge
+// "level by level" (the larger of a_l, b_l, then the smaller, for l = 0..3),
+// the merged sequence m0..m7 is known after the four level comparisons plus
+// three cross checks -- exactly the comparisons the reference merge makes --
+// and the merge loop becomes six fixed steps.  It also needs the loop to run
+// to the end (k <= 3 before the last step), so every limb is consumed, the
+// leftover fold is empty and the loop exit writes x[k] = u, x[k+1] = v.  That
+// covers operands of similar magnitude -- the MGS inner products, updates and
+// reductions.  Lanes outside it (zero or exhausted limbs mid-merge, widely
+// different exponents, early exits) run add_general; the branch is taken per
+// warp only when some lane needs it.
+XB_DEV r4 add(const r4& a, const r4& b) {
+    const bool f0 = dabs(a.c0) > dabs(b.c0), f1 = dabs(a.c1) > dabs(b.c1);
+    const bool f2 = dabs(a.c2) > dabs(b.c2), f3 = dabs(a.c3) > dabs(b.c3);
+    const double m0 = f0 ? a.c0 : b.c0, m1 = f0 ? b.c0 : a.c0;
+    const double m2 = f1 ? a.c1 : b.c1, m3 = f1 ? b.c1 : a.c1;
+    const double m4 = f2 ? a.c2 : b.c2, m5 = f2 ? b.c2 : a.c2;
+    const double m6 = f3 ? a.c3 : b.c3, m7 = f3 ? b.c3 : a.c3;
+    // the smaller limb of level l beats both limbs of level l+1 strictly: then
+    // the reference's comparison against the successor of the taken limb
+    // picks it (|a_{l+1}| > |b_l| is false, resp. |a_l| > |b_{l+1}| is true)
+    bool ok = (dabs(m1) > dabs(m2)) && (dabs(m3) > dabs(m4)) && (dabs(m5) > dabs(m6));
+    double u, v;
+    quick_two_sum(m0, m1, u, v);
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+    int k = 0;
+    qadd_step<0>(u, v, m2, k, x0, x1, x2, x3);
+    qadd_step<1>(u, v, m3, k, x0, x1, x2, x3);
+    qadd_step<2>(u, v, m4, k, x0, x1, x2, x3);
+    qadd_step<3>(u, v, m5, k, x0, x1, x2, x3);
+    qadd_step<3>(u, v, m6, k, x0, x1, x2, x3);
+    ok = ok && (k <= 3);
+    qadd_step<3>(u, v, m7, k, x0, x1, x2, x3);
+    // loop exit with everything consumed: x[k] = u; if (k < 3) x[k + 1] = v
+    x0 = (k == 0) ? u : x0;
+    x1 = (k == 1) ? u : ((k == 0) ? v : x1);
+    x2 = (k == 2) ? u : ((k == 1) ? v : x2);
+    x3 = (k == 3) ? u : ((k == 2) ? v : x3);
+    if (!ok) return add_general(a, b);
+    renorm4_fast(x0, x1, x2, x3);
     return {x0, x1, x2, x3};
 }
 XB_DEV r4 neg(const r4& a) { return {-a.c0, -a.c1, -a.c2, -a.c3}; }  // :259-261
@@ -438,7 +569,7 @@ XB_DEV r4 mul_pwr2(const r4& a, double p2) {  // :341-343
 // quad_double.hpp:359-370
 XB_DEV r4 rsqrt_ref(const r4& a) {
     if (a.c0 == 0.0 && a.c1 == 0.0 && a.c2 == 0.0 && a.c3 == 0.0) return {0.0, 0.0, 0.0, 0.0};
-    r4 x = make4(__ddiv_rn(1.0, __dsqrt_rn(a.c0)));
+    r4 x = make4(ddiv(1.0, dsqrt(a.c0)));
 #pragma unroll 1
     for (int it = 0; it < 2; ++it) {
         r4 t = mul(a, x);
@@ -487,15 +618,15 @@ struct recip_t<r4> {
 
 // plain IEEE division for double (real_type.hpp: no checked funnel)
 XB_DEV recip_t<r1> recip(const r1& b, int& status) { return {b.c0}; }
-XB_DEV r1 div_plain(const r1& a, const r1& b) { return {__ddiv_rn(a.c0, b.c0)}; }
-XB_DEV r1 divide(const r1& a, const r1& b, const recip_t<r1>& rc) { return {__ddiv_rn(a.c0, rc.b)}; }
+XB_DEV r1 div_plain(const r1& a, const r1& b) { return {ddiv(a.c0, b.c0)}; }
+XB_DEV r1 divide(const r1& a, const r1& b, const recip_t<r1>& rc) { return {ddiv(a.c0, rc.b)}; }
 
 XB_DEV recip_t<r2> recip(const r2& b, int& status) {
     if (b.c0 == 0.0) {
         status = 3;
         return {{0.0, 0.0}};
     }
-    double x0 = __ddiv_rn(1.0, b.c0);
+    double x0 = ddiv(1.0, b.c0);
     if (!finite(x0)) status = 2;
     r2 e = sub(make2(1.0), dd_mul_d(b, x0));
     return {dd_add_d(dd_mul_d(e, x0), x0)};
@@ -511,7 +642,7 @@ XB_DEV recip_t<r4> recip(const r4& b, int& status) {
         status = 3;
         return {{0.0, 0.0, 0.0, 0.0}};
     }
-    double seed = __ddiv_rn(1.0, b.c0);
+    double seed = ddiv(1.0, b.c0);
     if (!finite(seed)) status = 2;
     r4 x = make4(seed);
 #pragma unroll 1
@@ -579,6 +710,47 @@ XB_DEV cx<R> cdiv(const cx<R>& a, const cx<R>& b, int& status) {
 template <class R>
 XB_DEV bool cfinite(const cx<R>& z) {
     return finite(head(z.re)) && finite(head(z.im));
+}
+
+// ---- limb load / store with a plane stride ------------------------------------
+template <int L>
+using real_t = typename real_of<L>::type;
+
+template <int L>
+XB_DEV void load_real(const double* p, int stride, real_t<L>& v);
+template <>
+XB_DEV void load_real<1>(const double* p, int stride, r1& v) {
+    v.c0 = p[0];
+}
+template <>
+XB_DEV void load_real<2>(const double* p, int stride, r2& v) {
+    v.c0 = p[0];
+    v.c1 = p[stride];
+}
+template <>
+XB_DEV void load_real<4>(const double* p, int stride, r4& v) {
+    v.c0 = p[0];
+    v.c1 = p[stride];
+    v.c2 = p[2 * stride];
+    v.c3 = p[3 * stride];
+}
+template <int L>
+XB_DEV void store_real(double* p, int stride, const real_t<L>& v);
+template <>
+XB_DEV void store_real<1>(double* p, int stride, const r1& v) {
+    p[0] = v.c0;
+}
+template <>
+XB_DEV void store_real<2>(double* p, int stride, const r2& v) {
+    p[0] = v.c0;
+    p[stride] = v.c1;
+}
+template <>
+XB_DEV void store_real<4>(double* p, int stride, const r4& v) {
+    p[0] = v.c0;
+    p[stride] = v.c1;
+    p[2 * stride] = v.c2;
+    p[3 * stride] = v.c3;
 }
 
 }  // namespace xb

@@ -23,7 +23,7 @@ struct smith_prep {
 
 // Store/load the prep record (3L+1 doubles) in global scratch.
 template <int L>
-XB_DEV void prep_store(double* p, const smith_prep<L>& s) {
+XB_DEVICE void prep_store(double* p, const smith_prep<L>& s) {
     store_real<L>(p, 1, s.t);
     store_real<L>(p + L, 1, s.d);
     if constexpr (L == 1) p[2] = s.rc.b;
@@ -32,7 +32,7 @@ XB_DEV void prep_store(double* p, const smith_prep<L>& s) {
     p[3 * L] = (double)(s.br | (s.code << 4));
 }
 template <int L>
-XB_DEV smith_prep<L> prep_load(const double* p) {
+XB_DEVICE smith_prep<L> prep_load(const double* p) {
     smith_prep<L> s;
     load_real<L>(p, 1, s.t);
     load_real<L>(p + L, 1, s.d);
@@ -46,21 +46,21 @@ XB_DEV smith_prep<L> prep_load(const double* p) {
 }
 
 template <int L>
-XB_DEV cx<real_t<L>> load_aos(const double* p) {
+XB_DEVICE cx<real_t<L>> load_aos(const double* p) {
     cx<real_t<L>> z;
     load_real<L>(p, 1, z.re);
     load_real<L>(p + L, 1, z.im);
     return z;
 }
 template <int L>
-XB_DEV void store_aos(double* p, const cx<real_t<L>>& z) {
+XB_DEVICE void store_aos(double* p, const cx<real_t<L>>& z) {
     store_real<L>(p, 1, z.re);
     store_real<L>(p + L, 1, z.im);
 }
 
 // x = Smith(xk / d) given the divisor-only prep (complex.hpp:50-57).
 template <int L>
-XB_DEV cx<real_t<L>> smith_apply(const cx<real_t<L>>& a, const smith_prep<L>& s) {
+XB_DEVICE cx<real_t<L>> smith_apply(const cx<real_t<L>>& a, const smith_prep<L>& s) {
     using R = real_t<L>;
     if (s.br) {
         R nre = add(a.re, mul(a.im, s.t));
@@ -76,7 +76,7 @@ XB_DEV cx<real_t<L>> smith_apply(const cx<real_t<L>>& a, const smith_prep<L>& s)
 // prep: global scratch n*(3L+1).  Records errors into *key (shared) with
 // positions pos_base + (n-1-k).  Returns (uniformly) true on error.
 template <int L>
-XB_DEV bool cta_back_substitute(int n, const double* r, const double* y, double* xs, double* prep,
+XB_DEVICE bool cta_back_substitute(int n, const double* r, const double* y, double* xs, double* prep,
                                 unsigned long long* key, long long pos_base) {
     using R = real_t<L>;
     using C = cx<R>;

@@ -19,122 +19,82 @@
 
 namespace xb {
 
-template <int L>
-using real_t = typename real_of<L>::type;
-
-template <int L>
-XB_DEV void load_real(const double* p, int stride, real_t<L>& v);
-template <>
-XB_DEV void load_real<1>(const double* p, int stride, r1& v) {
-    v.c0 = p[0];
-}
-template <>
-XB_DEV void load_real<2>(const double* p, int stride, r2& v) {
-    v.c0 = p[0];
-    v.c1 = p[stride];
-}
-template <>
-XB_DEV void load_real<4>(const double* p, int stride, r4& v) {
-    v.c0 = p[0];
-    v.c1 = p[stride];
-    v.c2 = p[2 * stride];
-    v.c3 = p[3 * stride];
-}
-template <int L>
-XB_DEV void store_real(double* p, int stride, const real_t<L>& v);
-template <>
-XB_DEV void store_real<1>(double* p, int stride, const r1& v) {
-    p[0] = v.c0;
-}
-template <>
-XB_DEV void store_real<2>(double* p, int stride, const r2& v) {
-    p[0] = v.c0;
-    p[stride] = v.c1;
-}
-template <>
-XB_DEV void store_real<4>(double* p, int stride, const r4& v) {
-    p[0] = v.c0;
-    p[stride] = v.c1;
-    p[2 * stride] = v.c2;
-    p[3 * stride] = v.c3;
-}
-
 // Column addressing: plane stride LD = 32*rpl doubles, column = 2L planes.
 // rpl (rows per lane) is a runtime power of two.
 template <int L>
 struct colfmt {
     int rpl, LD, COL;
-    XB_DEV colfmt(int rows_per_lane) : rpl(rows_per_lane), LD(32 * rows_per_lane), COL(2 * L * 32 * rows_per_lane) {}
-    XB_DEV static int off(int t, int lane) { return t * 32 + lane; }
-    XB_DEV cx<real_t<L>> load(const double* col, int t, int lane) const {
+    XB_DEVICE colfmt(int rows_per_lane) : rpl(rows_per_lane), LD(32 * rows_per_lane), COL(2 * L * 32 * rows_per_lane) {}
+    XB_DEVICE static int off(int t, int lane) { return t * 32 + lane; }
+    XB_DEVICE cx<real_t<L>> load(const double* col, int t, int lane) const {
         cx<real_t<L>> z;
         load_real<L>(col + off(t, lane), LD, z.re);
         load_real<L>(col + L * LD + off(t, lane), LD, z.im);
         return z;
     }
-    XB_DEV void store(double* col, int t, int lane, const cx<real_t<L>>& z) const {
+    XB_DEVICE void store(double* col, int t, int lane, const cx<real_t<L>>& z) const {
         store_real<L>(col + off(t, lane), LD, z.re);
         store_real<L>(col + L * LD + off(t, lane), LD, z.im);
     }
     // row index -> offset inside a plane
-    XB_DEV int row_off(int row) const { return (row % rpl) * 32 + row / rpl; }
+    XB_DEVICE int row_off(int row) const { return (row % rpl) * 32 + row / rpl; }
 };
 
 template <class R>
-XB_DEV cx<R> shfl_down(const cx<R>& v, int o);
+XB_DEVICE cx<R> shfl_down(const cx<R>& v, int o);
 template <class R>
-XB_DEV R shfl_down_r(const R& v, int o);
+XB_DEVICE R shfl_down_r(const R& v, int o);
 template <>
-XB_DEV r1 shfl_down_r<r1>(const r1& v, int o) {
+XB_DEVICE r1 shfl_down_r<r1>(const r1& v, int o) {
     return {__shfl_down_sync(0xffffffffu, v.c0, o)};
 }
 template <>
-XB_DEV r2 shfl_down_r<r2>(const r2& v, int o) {
+XB_DEVICE r2 shfl_down_r<r2>(const r2& v, int o) {
     return {__shfl_down_sync(0xffffffffu, v.c0, o), __shfl_down_sync(0xffffffffu, v.c1, o)};
 }
 template <>
-XB_DEV r4 shfl_down_r<r4>(const r4& v, int o) {
+XB_DEVICE r4 shfl_down_r<r4>(const r4& v, int o) {
     return {__shfl_down_sync(0xffffffffu, v.c0, o), __shfl_down_sync(0xffffffffu, v.c1, o),
             __shfl_down_sync(0xffffffffu, v.c2, o), __shfl_down_sync(0xffffffffu, v.c3, o)};
 }
 template <class R>
-XB_DEV R shfl_idx_r(const R& v, int src);
+XB_DEVICE R shfl_idx_r(const R& v, int src);
 template <>
-XB_DEV r1 shfl_idx_r<r1>(const r1& v, int s) {
+XB_DEVICE r1 shfl_idx_r<r1>(const r1& v, int s) {
     return {__shfl_sync(0xffffffffu, v.c0, s)};
 }
 template <>
-XB_DEV r2 shfl_idx_r<r2>(const r2& v, int s) {
+XB_DEVICE r2 shfl_idx_r<r2>(const r2& v, int s) {
     return {__shfl_sync(0xffffffffu, v.c0, s), __shfl_sync(0xffffffffu, v.c1, s)};
 }
 template <>
-XB_DEV r4 shfl_idx_r<r4>(const r4& v, int s) {
+XB_DEVICE r4 shfl_idx_r<r4>(const r4& v, int s) {
     return {__shfl_sync(0xffffffffu, v.c0, s), __shfl_sync(0xffffffffu, v.c1, s),
             __shfl_sync(0xffffffffu, v.c2, s), __shfl_sync(0xffffffffu, v.c3, s)};
 }
 template <class R>
-XB_DEV cx<R> shfl_down_c(const cx<R>& v, int o) {
+XB_DEVICE cx<R> shfl_down_c(const cx<R>& v, int o) {
     return {shfl_down_r(v.re, o), shfl_down_r(v.im, o)};
 }
 template <class R>
-XB_DEV cx<R> shfl_idx_c(const cx<R>& v, int s) {
+XB_DEVICE cx<R> shfl_idx_c(const cx<R>& v, int s) {
     return {shfl_idx_r(v.re, s), shfl_idx_r(v.im, s)};
 }
 
 template <class R>
-XB_DEV R vadd(const R& a, const R& b) {
+XB_DEVICE R vadd(const R& a, const R& b) {
     return add(a, b);
 }
 template <class R>
-XB_DEV cx<R> vadd(const cx<R>& a, const cx<R>& b) {
+XB_DEVICE cx<R> vadd(const cx<R>& a, const cx<R>& b) {
     return cadd(a, b);
 }
 template <class R>
-XB_DEV R vshfl_down(const R& v, int o) {
+XB_DEVICE R vshfl_down(const R& v, int o) {
     return shfl_down_r(v, o);
 }
 template <class R>
-XB_DEV cx<R> vshfl_down(const cx<R>& v, int o) {
+XB_DEVICE cx<R> vshfl_down(const cx<R>& v, int o) {
     return shfl_down_c(v, o);
 }
 
@@ -146,7 +106,7 @@ XB_DEV cx<R> vshfl_down(const cx<R>& v, int o) {
 // folds its stack right to left, i.e. tree_reduce's skipped partners.
 template <int LV, int l, class V>
 struct counter_merge {
-    XB_DEV static void push(V (&st)[LV], V v, int t) {
+    XB_DEVICE static void push(V (&st)[LV], V v, int t) {
         if ((t >> l) & 1) {
             v = vadd(st[l], v);
             counter_merge<LV, l + 1, V>::push(st, v, t);
@@ -157,11 +117,11 @@ struct counter_merge {
 };
 template <int LV, class V>
 struct counter_merge<LV, LV, V> {
-    XB_DEV static void push(V (&)[LV], V, int) {}
+    XB_DEVICE static void push(V (&)[LV], V, int) {}
 };
 
 template <int LV, class V, class LeafFn>
-XB_DEV V lane_tree(int cnt, LeafFn leaf) {
+XB_DEVICE V lane_tree(int cnt, LeafFn leaf) {
     V st[LV];
 #pragma unroll 1
     for (int t = 0; t < cnt; ++t) counter_merge<LV, 0, V>::push(st, leaf(t), t);
@@ -184,7 +144,7 @@ XB_DEV V lane_tree(int cnt, LeafFn leaf) {
 // Cross-lane levels: strides RPL, 2RPL, ... as shuffle offsets 1, 2, 4, ...
 // Lane 0 ends with the total; every lane returns it (broadcast).
 template <class V>
-XB_DEV V warp_tree(V acc, int lane, int m, int rpl) {
+XB_DEVICE V warp_tree(V acc, int lane, int m, int rpl) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         V other = vshfl_down(acc, o);

@@ -37,16 +37,16 @@ constexpr int kGridWarps = kGridThreads / 32;
 template <int L>
 struct gridfmt {
     int rpt, LD, COL;
-    XB_DEV explicit gridfmt(int r) : rpt(r), LD(kGridThreads * r), COL(2 * L * kGridThreads * r) {}
-    XB_DEV static int off(int i, int t) { return i * kGridThreads + t; }
-    XB_DEV int row_off(int row) const { return (row % rpt) * kGridThreads + row / rpt; }
-    XB_DEV cx<real_t<L>> load(const double* col, int i, int t) const {
+    XB_DEVICE explicit gridfmt(int r) : rpt(r), LD(kGridThreads * r), COL(2 * L * kGridThreads * r) {}
+    XB_DEVICE static int off(int i, int t) { return i * kGridThreads + t; }
+    XB_DEVICE int row_off(int row) const { return (row % rpt) * kGridThreads + row / rpt; }
+    XB_DEVICE cx<real_t<L>> load(const double* col, int i, int t) const {
         cx<real_t<L>> z;
         load_real<L>(col + off(i, t), LD, z.re);
         load_real<L>(col + L * LD + off(i, t), LD, z.im);
         return z;
     }
-    XB_DEV cx<real_t<L>> load_cg(const double* col, int i, int t) const {
+    XB_DEVICE cx<real_t<L>> load_cg(const double* col, int i, int t) const {
         // L2-coherent read of a column another CTA published
         cx<real_t<L>> z;
         const double* p = col + off(i, t);
@@ -57,7 +57,7 @@ struct gridfmt {
         load_real<L>(v + L, 1, z.im);
         return z;
     }
-    XB_DEV void store(double* col, int i, int t, const cx<real_t<L>>& z) const {
+    XB_DEVICE void store(double* col, int i, int t, const cx<real_t<L>>& z) const {
         store_real<L>(col + off(i, t), LD, z.re);
         store_real<L>(col + L * LD + off(i, t), LD, z.im);
     }
@@ -67,7 +67,7 @@ struct gridfmt {
 // partials (strides 32*rpt, 64*rpt, 128*rpt) by warp 0.  Every thread gets
 // the total.  `red` is a shared scratch of kGridWarps+1 values.
 template <int LV, class V, class LeafFn>
-XB_DEV V cta_tree(int m, int rpt, V* red, LeafFn leaf) {
+XB_DEVICE V cta_tree(int m, int rpt, V* red, LeafFn leaf) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int cnt = m - tid * rpt;
     cnt = cnt < 0 ? 0 : (cnt > rpt ? rpt : cnt);
@@ -95,12 +95,12 @@ XB_DEV V cta_tree(int m, int rpt, V* red, LeafFn leaf) {
     return red[kGridWarps];
 }
 
-XB_DEV int ld_acquire(const int* p) {
+XB_DEVICE int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-XB_DEV void st_release(int* p, int v) {
+XB_DEVICE void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 

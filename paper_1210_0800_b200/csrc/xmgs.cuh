@@ -30,14 +30,14 @@ struct mgs_warp {
     using C = cx<R>;
     using F = colfmt<L>;
 
-    XB_DEV static int lane_rows(int lane, int m, int rpl) {
+    XB_DEVICE static int lane_rows(int lane, int m, int rpl) {
         int c = m - lane * rpl;
         return c < 0 ? 0 : (c > rpl ? rpl : c);
     }
 
     // Re(a^H a) over the fixed tree (mgs.hpp:38-42, reduction.hpp:45-51);
     // result broadcast to every lane.
-    XB_DEV static R col_sq(const F& f, const double* col, int lane, int m) {
+    XB_DEVICE static R col_sq(const F& f, const double* col, int lane, int m) {
         const int cnt = lane_rows(lane, m, f.rpl);
         R acc = lane_tree<LV, R>(cnt, [&](int t) {
             C a = f.load(col, t, lane);
@@ -48,7 +48,7 @@ struct mgs_warp {
     }
 
     // q^H a over the fixed tree; broadcast.
-    XB_DEV static C dot(const F& f, const double* q, const double* col, int lane, int m) {
+    XB_DEVICE static C dot(const F& f, const double* q, const double* col, int lane, int m) {
         const int cnt = lane_rows(lane, m, f.rpl);
         C acc = lane_tree<LV, C>(cnt, [&](int t) {
             return cmul(cconj(f.load(q, t, lane)), f.load(col, t, lane));
@@ -59,7 +59,7 @@ struct mgs_warp {
 
     // remove_projection (mgs.hpp:57-61): r = q^H a; a_i -= r * q_i.
     // Returns false if any produced value is not finite.
-    XB_DEV static bool remove_projection(const F& f, const double* q, double* col, int lane, int m,
+    XB_DEVICE static bool remove_projection(const F& f, const double* q, double* col, int lane, int m,
                                          C& r) {
         r = dot(f, q, col, lane, m);
         bool ok = cfinite(r);
@@ -76,7 +76,7 @@ struct mgs_warp {
 
     // normalize_column (mgs.hpp:46-53) into col and the shared pivot slot.
     // code: 0 ok, 1 breakdown, 2 overflow, 3 domain.
-    XB_DEV static int normalize(const F& f, double* col, double* slot, const R& thr, int lane, int m,
+    XB_DEVICE static int normalize(const F& f, double* col, double* slot, const R& thr, int lane, int m,
                                 R& rkk) {
         R s = col_sq(f, col, lane, m);
         rkk = rsqrt_ref(s);
