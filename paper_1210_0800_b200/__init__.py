@@ -43,7 +43,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-library_path = os.path.join(HERE, "libxqr_b200.so")
+library_path = os.environ.get("XQR_B200_LIB") or os.path.join(HERE, "libxqr_b200.so")
 
 
 # ---- errors (errors.hpp:13-51) ------------------------------------------------

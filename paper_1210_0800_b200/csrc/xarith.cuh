@@ -26,11 +26,40 @@ namespace xb {
 
 #ifdef __CUDACC__
 #define XB_DEV __host__ __device__ __forceinline__
-#define XB_NOINLINE __host__ __device__ __noinline__
+#define XB_NOINLINE inline __host__ __device__ __noinline__
 #define XB_DEVICE __device__ __forceinline__  // device-only helpers (shuffles, ...)
 #else
 #define XB_DEV inline
 #define XB_NOINLINE
+#endif
+
+// Code-size control.  A quad-double kernel inlines hundreds of qd adds and
+// multiplies; fully inlined, the hot loop outgrows the instruction cache
+// (ncu: stall_no_inst).  XB_CALLS is a bit mask of the qd operations that
+// become real calls: 1 = qd add, 2 = complex qd multiply and add, 4 = qd
+// multiply.
+#ifndef XB_CALLS
+#define XB_CALLS 7
+#endif
+#if defined(__CUDACC__)
+#define XB_CALL_IF inline __host__ __device__ __noinline__
+#else
+#define XB_CALL_IF inline
+#endif
+#if (XB_CALLS & 1)
+#define XB_OP1 XB_CALL_IF
+#else
+#define XB_OP1 XB_DEV
+#endif
+#if (XB_CALLS & 2)
+#define XB_OP2 XB_CALL_IF
+#else
+#define XB_OP2 XB_DEV
+#endif
+#if (XB_CALLS & 4)
+#define XB_OP3 XB_CALL_IF
+#else
+#define XB_OP3 XB_DEV
 #endif
 
 #ifdef __CUDA_ARCH__
@@ -458,7 +487,7 @@ XB_DEV void renorm4_fast(double& c0, double& c1, double& c2, double& c3) {
 // reductions.  Lanes outside it (zero or exhausted limbs mid-merge, widely
 // different exponents, early exits) run add_general; the branch is taken per
 // warp only when some lane needs it.
-XB_DEV r4 add(const r4& a, const r4& b) {
+XB_OP1 r4 add(const r4& a, const r4& b) {
     const bool f0 = dabs(a.c0) > dabs(b.c0), f1 = dabs(a.c1) > dabs(b.c1);
     const bool f2 = dabs(a.c2) > dabs(b.c2), f3 = dabs(a.c3) > dabs(b.c3);
     const double m0 = f0 ? a.c0 : b.c0, m1 = f0 ? b.c0 : a.c0;
@@ -505,7 +534,7 @@ XB_DEV r4 renormalize(const r4& a) {
 XB_DEV r4 sub(const r4& a, const r4& b) { return add(a, neg(b)); }     // :263
 
 // quad_double.hpp:267-338
-XB_DEV r4 mul(const r4& a, const r4& b) {
+XB_OP3 r4 mul(const r4& a, const r4& b) {
     double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5;
     two_prod(a.c0, b.c0, p0, q0);
     two_prod(a.c0, b.c1, p1, q1);
@@ -674,12 +703,20 @@ template <class R>
 XB_DEV cx<R> cadd(const cx<R>& a, const cx<R>& b) {  // :26-29
     return {add(a.re, b.re), add(a.im, b.im)};
 }
+template <>
+XB_OP2 cx<r4> cadd<r4>(const cx<r4>& a, const cx<r4>& b) {
+    return {add(a.re, b.re), add(a.im, b.im)};
+}
 template <class R>
 XB_DEV cx<R> csub(const cx<R>& a, const cx<R>& b) {  // :31-34
     return {sub(a.re, b.re), sub(a.im, b.im)};
 }
 template <class R>
 XB_DEV cx<R> cmul(const cx<R>& a, const cx<R>& b) {  // :41-44
+    return {sub(mul(a.re, b.re), mul(a.im, b.im)), add(mul(a.re, b.im), mul(a.im, b.re))};
+}
+template <>
+XB_OP2 cx<r4> cmul<r4>(const cx<r4>& a, const cx<r4>& b) {
     return {sub(mul(a.re, b.re), mul(a.im, b.im)), add(mul(a.re, b.im), mul(a.im, b.re))};
 }
 // Re(conj(a) * b): the real half of cmul(cconj(a), b), same ops.

@@ -11,7 +11,10 @@ constexpr int kWarps = 4;
 // Minimum resident CTAs per SM requested from ptxas (caps registers).
 template <int L, int LV>
 constexpr int min_blocks() {
-    return L == 4 ? (LV <= 3 ? 3 : 1) : (LV <= 3 ? 4 : 2);
+#ifndef XB_MINB4
+#define XB_MINB4 4
+#endif
+    return L == 4 ? (LV <= 3 ? XB_MINB4 : 1) : (LV <= 3 ? 4 : 2);
 }
 
 template <int L, int LV, bool LSQ>
