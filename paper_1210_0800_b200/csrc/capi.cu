@@ -143,6 +143,8 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     const size_t o_nrm = plan.add(sizeof(double) * (size_t)ncol * limbs);
     const size_t o_flg = plan.add(sizeof(int) * (size_t)n);
     const size_t o_key = plan.add(sizeof(unsigned long long));
+    const char* trace_path = std::getenv("XQR_GRID_TRACE");  // dev instrumentation
+    const size_t o_trc = plan.add(trace_path ? sizeof(unsigned long long) * 4 * (size_t)(n + 1) : 0);
     cudaError_t e = ensure_arena(ctx, scratch_off + plan.total + 256);
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
     p.ws = reinterpret_cast<double*>(at(ctx, scratch_off + o_ws));
@@ -150,6 +152,8 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     p.norms = reinterpret_cast<double*>(at(ctx, scratch_off + o_nrm));
     p.flags = reinterpret_cast<int*>(at(ctx, scratch_off + o_flg));
     p.key = reinterpret_cast<unsigned long long*>(at(ctx, scratch_off + o_key));
+    p.trace = trace_path ? reinterpret_cast<unsigned long long*>(at(ctx, scratch_off + o_trc)) : nullptr;
+    if (p.trace) cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * 4 * (size_t)(n + 1), ctx->stream);
     cudaMemsetAsync(p.flags, 0, sizeof(int) * (size_t)n, ctx->stream);
     cudaMemsetAsync(p.key, 0xFF, sizeof(unsigned long long), ctx->stream);
     const int grid = std::min(ncol, ctx->num_sms);
@@ -163,6 +167,17 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     ctx->timed = timed;
     ctx->launches += 1;
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "grid kernel launch");
+    if (p.trace) {
+        std::vector<unsigned long long> h(4 * (size_t)(n + 1));
+        cudaMemcpyAsync(h.data(), p.trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
+                        ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        if (FILE* fp = std::fopen(trace_path, "w")) {
+            for (int j = 0; j <= n; ++j)
+                std::fprintf(fp, "%d %llu %llu %llu %llu\n", j, h[4 * j], h[4 * j + 1], h[4 * j + 2], h[4 * j + 3]);
+            std::fclose(fp);
+        }
+    }
     return 0;
 }
 

@@ -33,11 +33,17 @@ namespace xb {
 #define XB_NOINLINE
 #endif
 
-// Code-size control.  A quad-double kernel inlines hundreds of qd adds and
-// multiplies; fully inlined, the hot loop outgrows the instruction cache
-// (ncu: stall_no_inst).  XB_CALLS is a bit mask of the qd operations that
-// become real calls: 1 = qd add, 2 = complex qd multiply and add, 4 = qd
-// multiply.
+// Code-size and latency control.  Every quad-double add and multiply has a
+// straight-line fast path (always inlined, so independent operations
+// interleave) and a general path that replays the reference's branches for
+// the lanes the fast path cannot take.  XB_CALLS is a bit mask: 1 = the
+// general paths are real calls (they are rare; inlined they would dominate
+// the code size), 2 = the complex quad-double operations and the scalar
+// sqrt / reciprocal are real calls, 4 = the real quad-double add and
+// multiply are real calls (no interleaving of independent operations, but
+// the smallest code: the throughput-bound batched kernel runs many warps and
+// needs its hot loop to fit the instruction cache; the latency-bound grid
+// kernel wants the interleaving).
 #ifndef XB_CALLS
 #define XB_CALLS 7
 #endif
@@ -47,9 +53,9 @@ namespace xb {
 #define XB_CALL_IF inline
 #endif
 #if (XB_CALLS & 1)
-#define XB_OP1 XB_CALL_IF
+#define XB_GEN XB_CALL_IF
 #else
-#define XB_OP1 XB_DEV
+#define XB_GEN XB_DEV
 #endif
 #if (XB_CALLS & 2)
 #define XB_OP2 XB_CALL_IF
@@ -57,9 +63,9 @@ namespace xb {
 #define XB_OP2 XB_DEV
 #endif
 #if (XB_CALLS & 4)
-#define XB_OP3 XB_CALL_IF
+#define XB_OP4 XB_CALL_IF
 #else
-#define XB_OP3 XB_DEV
+#define XB_OP4 XB_DEV
 #endif
 
 #ifdef __CUDA_ARCH__
@@ -356,12 +362,14 @@ XB_DEV double pick4(int i, double x0, double x1, double x2, double x3) {
 // limb reads are register selects, never local-memory indexing.  This is the
 // general form; add() below runs it only for the lanes its fast path cannot
 // take.
-#ifdef XB_GENERAL_NOINLINE
-XB_NOINLINE
+#ifdef XB_COUNT_GENERAL
+inline long g_add_general = 0, g_mul_general = 0, g_add_zt = 0;
+#define XB_COUNT(c) (++(c))
 #else
-XB_DEV
+#define XB_COUNT(c) ((void)0)
 #endif
-r4 add_general(const r4& a, const r4& b) {
+XB_GEN r4 add_general(const r4& a, const r4& b) {
+    XB_COUNT(g_add_general);
     int i = 0, j = 0, k = 0;
     double u, v;
     double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
@@ -450,27 +458,45 @@ XB_DEV void qadd_step(double& u, double& v, double s, int& k, double& x0, double
 }
 
 // renorm4 (quad_double.hpp:157-200) for the common case -- no infinity, no
-// zero error term along the way -- as straight-line code; any other lane
-// runs the reference branch tree.
-XB_DEV void renorm4_fast(double& c0, double& c1, double& c2, double& c3) {
-    double t, e, s0, s1, s2, s3, t1, e1;
+// zero error term along the way -- as straight-line code.  ok = false: the
+// reference takes another branch; the caller replays the general path.
+XB_DEV void renorm4_fast(double& c0, double& c1, double& c2, double& c3, bool& ok) {
+    double t, e, s0, s1, d2, d3, t1, e1, u2, u3;
+    const bool inf0 = is_inf(c0);
     quick_two_sum(c2, c3, t, e);
-    s3 = e;
+    d3 = e;
     quick_two_sum(c1, t, t, e);
-    s2 = e;
+    d2 = e;
     quick_two_sum(c0, t, s0, s1);
     // s1 != 0 -> quick_two_sum(s1, c2'); s2' != 0 -> quick_two_sum(s2', c3')
-    quick_two_sum(s1, s2, t1, e1);
-    double u2, u3;
-    quick_two_sum(e1, s3, u2, u3);
-    if (!is_inf(c0) && s1 != 0.0 && e1 != 0.0) {
-        c0 = s0;
-        c1 = t1;
-        c2 = u2;
-        c3 = u3;
-    } else {
-        renorm4(c0, c1, c2, c3);
-    }
+    quick_two_sum(s1, d2, t1, e1);
+    quick_two_sum(e1, d3, u2, u3);
+    ok = !inf0 && s1 != 0.0 && e1 != 0.0;
+    c0 = s0;
+    c1 = t1;
+    c2 = u2;
+    c3 = u3;
+}
+
+// renorm (five components, quad_double.hpp:78-154), common case likewise:
+// every zero test of the reference tree takes its "non-zero" side.
+XB_DEV void renorm5_fast(double& c0, double& c1, double& c2, double& c3, double c4, bool& ok) {
+    double t, e, d2, d3, d4, s0, s1, s1b, s2, s2b, s3;
+    const bool inf0 = is_inf(c0);
+    quick_two_sum(c3, c4, t, e);
+    d4 = e;
+    quick_two_sum(c2, t, t, e);
+    d3 = e;
+    quick_two_sum(c1, t, t, e);
+    d2 = e;
+    quick_two_sum(c0, t, s0, s1);
+    quick_two_sum(s1, d2, s1b, s2);
+    quick_two_sum(s2, d3, s2b, s3);
+    ok = !inf0 && s1 != 0.0 && s2 != 0.0 && s3 != 0.0;
+    c0 = s0;
+    c1 = s1b;
+    c2 = s2b;
+    c3 = dadd(s3, d4);
 }
 
 // quad_double.hpp:216-257, the same operations on the same operands in the
@@ -486,8 +512,10 @@ XB_DEV void renorm4_fast(double& c0, double& c1, double& c2, double& c3) {
 // covers operands of similar magnitude -- the MGS inner products, updates and
 // reductions.  Lanes outside it (zero or exhausted limbs mid-merge, widely
 // different exponents, early exits) run add_general; the branch is taken per
-// warp only when some lane needs it.
-XB_OP1 r4 add(const r4& a, const r4& b) {
+// warp only when some lane needs it.  add_fast() reports whether its result
+// is the reference's (ok); callers with independent adds run all fast paths
+// first and branch once.
+XB_DEV r4 add_fast(const r4& a, const r4& b, bool& okr) {
     const bool f0 = dabs(a.c0) > dabs(b.c0), f1 = dabs(a.c1) > dabs(b.c1);
     const bool f2 = dabs(a.c2) > dabs(b.c2), f3 = dabs(a.c3) > dabs(b.c3);
     const double m0 = f0 ? a.c0 : b.c0, m1 = f0 ? b.c0 : a.c0;
@@ -514,9 +542,69 @@ XB_OP1 r4 add(const r4& a, const r4& b) {
     x1 = (k == 1) ? u : ((k == 0) ? v : x1);
     x2 = (k == 2) ? u : ((k == 1) ? v : x2);
     x3 = (k == 3) ? u : ((k == 2) ? v : x3);
-    if (!ok) return add_general(a, b);
-    renorm4_fast(x0, x1, x2, x3);
+    bool okn;
+    renorm4_fast(x0, x1, x2, x3, okn);
+    okr = ok && okn;
     return {x0, x1, x2, x3};
+}
+// Second fast path, for an operand whose three lower limbs are zero (a
+// double widened to quad-double: the constants and seeds of the Newton
+// iterations, the generator's widened inputs).  The reference merge then
+// takes the two heads, the other operand's lower limbs, and the zeros last:
+//   a = (x,0,0,0): heads, b1, b2, b3, a1, a2, a3  (a0 taken second needs
+//                  |a0| > |b1|)
+//   b = (y,0,0,0): heads, a1, a2, a3, b1, b2, b3  (needs |a1|, |a2|, |a3| > 0,
+//                  and a0 taken first needs !(|a1| > |b0|), second |a0| > 0)
+// again exactly the comparisons the reference makes.
+XB_DEV r4 add_zt_fast(const r4& a, const r4& b, bool& okr) {
+    const bool f0 = dabs(a.c0) > dabs(b.c0);
+    const bool ta = (a.c1 == 0.0) && (a.c2 == 0.0) && (a.c3 == 0.0);
+    const bool tb = (b.c1 == 0.0) && (b.c2 == 0.0) && (b.c3 == 0.0);
+    bool ok;
+    if (ta) {
+        ok = f0 || (dabs(a.c0) > dabs(b.c1));
+    } else {
+        ok = tb && (dabs(a.c1) > 0.0) && (dabs(a.c2) > 0.0) && (dabs(a.c3) > 0.0) &&
+             (f0 ? !(dabs(a.c1) > dabs(b.c0)) : (dabs(a.c0) > 0.0));
+    }
+    const double m0 = f0 ? a.c0 : b.c0, m1 = f0 ? b.c0 : a.c0;
+    const double m2 = ta ? b.c1 : a.c1, m3 = ta ? b.c2 : a.c2, m4 = ta ? b.c3 : a.c3;
+    const double m5 = ta ? a.c1 : b.c1, m6 = ta ? a.c2 : b.c2, m7 = ta ? a.c3 : b.c3;
+    double u, v;
+    quick_two_sum(m0, m1, u, v);
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+    int k = 0;
+    qadd_step<0>(u, v, m2, k, x0, x1, x2, x3);
+    qadd_step<1>(u, v, m3, k, x0, x1, x2, x3);
+    qadd_step<2>(u, v, m4, k, x0, x1, x2, x3);
+    qadd_step<3>(u, v, m5, k, x0, x1, x2, x3);
+    qadd_step<3>(u, v, m6, k, x0, x1, x2, x3);
+    ok = ok && (k <= 3);
+    qadd_step<3>(u, v, m7, k, x0, x1, x2, x3);
+    x0 = (k == 0) ? u : x0;
+    x1 = (k == 1) ? u : ((k == 0) ? v : x1);
+    x2 = (k == 2) ? u : ((k == 1) ? v : x2);
+    x3 = (k == 3) ? u : ((k == 2) ? v : x3);
+    bool okn;
+    renorm4_fast(x0, x1, x2, x3, okn);
+    okr = ok && okn;
+    return {x0, x1, x2, x3};
+}
+
+// Everything the fast paths do not cover: the zero-tail path, else the
+// reference merge (one call, so the inlined fast path stays small).
+XB_GEN r4 add_slow(const r4& a, const r4& b) {
+    bool ok;
+    r4 r = add_zt_fast(a, b, ok);
+    if (!ok) r = add_general(a, b);
+    return r;
+}
+
+XB_OP4 r4 add(const r4& a, const r4& b) {
+    bool ok;
+    r4 r = add_fast(a, b, ok);
+    if (!ok) r = add_slow(a, b);
+    return r;
 }
 XB_DEV r4 neg(const r4& a) { return {-a.c0, -a.c1, -a.c2, -a.c3}; }  // :259-261
 // renormalize (real_type.hpp:20, double_double.hpp:28-31, quad_double.hpp:209-213)
@@ -533,9 +621,11 @@ XB_DEV r4 renormalize(const r4& a) {
 }
 XB_DEV r4 sub(const r4& a, const r4& b) { return add(a, neg(b)); }     // :263
 
-// quad_double.hpp:267-338
-XB_OP3 r4 mul(const r4& a, const r4& b) {
-    double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5;
+// quad_double.hpp:267-338: every partial product to order u^3 through EFTs;
+// qmul_core stops before the final renormalisation.
+XB_DEV void qmul_core(const r4& a, const r4& b, double& p0, double& p1, double& s0, double& t0c,
+                      double& t1c) {
+    double q0, q1, p2, q2, p3, q3, p4, q4, p5, q5;
     two_prod(a.c0, b.c0, p0, q0);
     two_prod(a.c0, b.c1, p1, q1);
     two_prod(a.c1, b.c0, p2, q2);
@@ -547,7 +637,7 @@ XB_OP3 r4 mul(const r4& a, const r4& b) {
 
     three_sum(p2, q1, q2);
     three_sum(p3, p4, p5);
-    double s0, t0, s1, t1;
+    double t0, s1, t1;
     two_sum(p2, p3, s0, t0);
     two_sum(q1, p4, s1, t1);
     // (s2 = q2 + p5; s2 += t0 + t1 is dead in the reference: never read)
@@ -576,7 +666,6 @@ XB_OP3 r4 mul(const r4& a, const r4& b) {
     two_sum(t0b, r0, q3b, q4b);
     q4b = dadd(q4b, dadd(t1b, r1));
 
-    double t0c, t1c;
     two_sum(q3b, s1, t0c, t1c);
     t1c = dadd(t1c, q4b);
 
@@ -589,14 +678,32 @@ XB_OP3 r4 mul(const r4& a, const r4& b) {
     w = dadd(w, q9);
     t1c = dadd(t1c, w);
 
+}
+XB_DEV r4 mul_fast(const r4& a, const r4& b, bool& ok) {
+    double p0, p1, s0, t0c, t1c;
+    qmul_core(a, b, p0, p1, s0, t0c, t1c);
+    renorm5_fast(p0, p1, s0, t0c, t1c, ok);
+    return {p0, p1, s0, t0c};
+}
+XB_GEN r4 mul_general(const r4& a, const r4& b) {
+    XB_COUNT(g_mul_general);
+    double p0, p1, s0, t0c, t1c;
+    qmul_core(a, b, p0, p1, s0, t0c, t1c);
     renorm5(p0, p1, s0, t0c, t1c);
     return {p0, p1, s0, t0c};
 }
+XB_OP4 r4 mul(const r4& a, const r4& b) {
+    bool ok;
+    r4 r = mul_fast(a, b, ok);
+    if (!ok) r = mul_general(a, b);
+    return r;
+}
+
 XB_DEV r4 mul_pwr2(const r4& a, double p2) {  // :341-343
     return {dmul(a.c0, p2), dmul(a.c1, p2), dmul(a.c2, p2), dmul(a.c3, p2)};
 }
 // quad_double.hpp:359-370
-XB_DEV r4 rsqrt_ref(const r4& a) {
+XB_OP2 r4 rsqrt_ref(const r4& a) {
     if (a.c0 == 0.0 && a.c1 == 0.0 && a.c2 == 0.0 && a.c3 == 0.0) return {0.0, 0.0, 0.0, 0.0};
     r4 x = make4(ddiv(1.0, dsqrt(a.c0)));
 #pragma unroll 1
@@ -666,7 +773,7 @@ XB_DEV r2 divide(const r2& a, const r2& b, const recip_t<r2>& rc) {
     return add(q, mul(r, rc.x1));
 }
 
-XB_DEV recip_t<r4> recip(const r4& b, int& status) {
+XB_OP2 recip_t<r4> recip(const r4& b, int& status) {
     if (b.c0 == 0.0) {
         status = 3;
         return {{0.0, 0.0, 0.0, 0.0}};
@@ -699,30 +806,105 @@ template <class R>
 XB_DEV cx<R> cconj(const cx<R>& z) {  // complex.hpp:21-24
     return {z.re, neg(z.im)};
 }
+// Two independent operations: both fast paths first (they interleave), one
+// branch to the general paths.  Generic form for double / double-double.
 template <class R>
-XB_DEV cx<R> cadd(const cx<R>& a, const cx<R>& b) {  // :26-29
-    return {add(a.re, b.re), add(a.im, b.im)};
+struct rpair {
+    R x, y;
+};
+template <class R>
+XB_DEV rpair<R> add2(const R& a1, const R& b1, const R& a2, const R& b2) {
+    return {add(a1, b1), add(a2, b2)};
+}
+template <class R>
+XB_DEV rpair<R> mul2(const R& a1, const R& b1, const R& a2, const R& b2) {
+    return {mul(a1, b1), mul(a2, b2)};
+}
+#if !(XB_CALLS & 4)
+template <>
+XB_DEV rpair<r4> add2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2) {
+    bool k1, k2;
+    rpair<r4> o{add_fast(a1, b1, k1), add_fast(a2, b2, k2)};
+    if (!(k1 && k2)) {
+        if (!k1) o.x = add_slow(a1, b1);
+        if (!k2) o.y = add_slow(a2, b2);
+    }
+    return o;
 }
 template <>
-XB_OP2 cx<r4> cadd<r4>(const cx<r4>& a, const cx<r4>& b) {
-    return {add(a.re, b.re), add(a.im, b.im)};
+XB_DEV rpair<r4> mul2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2) {
+    bool k1, k2;
+    rpair<r4> o{mul_fast(a1, b1, k1), mul_fast(a2, b2, k2)};
+    if (!(k1 && k2)) {
+        if (!k1) o.x = mul_general(a1, b1);
+        if (!k2) o.y = mul_general(a2, b2);
+    }
+    return o;
+}
+#endif
+
+template <class R>
+XB_DEV cx<R> cadd_t(const cx<R>& a, const cx<R>& b) {  // complex.hpp:26-29
+    rpair<R> o = add2(a.re, b.re, a.im, b.im);
+    return {o.x, o.y};
 }
 template <class R>
-XB_DEV cx<R> csub(const cx<R>& a, const cx<R>& b) {  // :31-34
-    return {sub(a.re, b.re), sub(a.im, b.im)};
+XB_DEV cx<R> csub_t(const cx<R>& a, const cx<R>& b) {  // :31-34 (a - b = a + (-b))
+    rpair<R> o = add2(a.re, neg(b.re), a.im, neg(b.im));
+    return {o.x, o.y};
 }
 template <class R>
-XB_DEV cx<R> cmul(const cx<R>& a, const cx<R>& b) {  // :41-44
-    return {sub(mul(a.re, b.re), mul(a.im, b.im)), add(mul(a.re, b.im), mul(a.im, b.re))};
+XB_DEV cx<R> csub(const cx<R>& a, const cx<R>& b) {
+    return csub_t(a, b);
 }
-template <>
-XB_OP2 cx<r4> cmul<r4>(const cx<r4>& a, const cx<r4>& b) {
-    return {sub(mul(a.re, b.re), mul(a.im, b.im)), add(mul(a.re, b.im), mul(a.im, b.re))};
+// complex.hpp:41-44: {a.re*b.re - a.im*b.im, a.re*b.im + a.im*b.re}; the four
+// products are independent, then the two sums.
+template <class R>
+XB_DEV cx<R> cmul_t(const cx<R>& a, const cx<R>& b) {
+    rpair<R> p = mul2(a.re, b.re, a.im, b.im);
+    rpair<R> q = mul2(a.re, b.im, a.im, b.re);
+    rpair<R> o = add2(p.x, neg(p.y), q.x, q.y);
+    return {o.x, o.y};
 }
+template <class R>
+XB_DEV cx<R> cadd(const cx<R>& a, const cx<R>& b) {
+    return cadd_t(a, b);
+}
+template <class R>
+XB_DEV cx<R> cmul(const cx<R>& a, const cx<R>& b) {
+    return cmul_t(a, b);
+}
+// quad-double: overloads (preferred over the templates) that can be calls
+XB_OP2 cx<r4> cadd(const cx<r4>& a, const cx<r4>& b) { return cadd_t(a, b); }
+XB_OP2 cx<r4> cmul(const cx<r4>& a, const cx<r4>& b) { return cmul_t(a, b); }
+template <class R>
+XB_DEV cx<R> csub_t(const cx<R>& a, const cx<R>& b);
+XB_OP2 cx<r4> csub(const cx<r4>& a, const cx<r4>& b) { return csub_t(a, b); }
 // Re(conj(a) * b): the real half of cmul(cconj(a), b), same ops.
 template <class R>
 XB_DEV R cdot_re(const cx<R>& a, const cx<R>& b) {
-    return sub(mul(a.re, b.re), mul(neg(a.im), b.im));
+    rpair<R> p = mul2(a.re, b.re, neg(a.im), b.im);
+    return sub(p.x, p.y);
+}
+XB_OP2 r4 cdot_re(const cx<r4>& a, const cx<r4>& b) {
+    rpair<r4> p = mul2(a.re, b.re, neg(a.im), b.im);
+    return sub(p.x, p.y);
+}
+// {a.re / b, a.im / b} with b's reciprocal prefix hoisted (div_real,
+// complex.hpp:61-65); the two tails interleave.
+template <class R>
+XB_DEV cx<R> cdivide_real(const cx<R>& a, const R& b, const recip_t<R>& rc) {
+    return {divide(a.re, b, rc), divide(a.im, b, rc)};
+}
+// quad-double: q = a*x; q = q + x*(a - b*q) (quad_double.hpp:352-353) for
+// both parts in lockstep
+XB_OP2 cx<r4> cdivide_real(const cx<r4>& a, const r4& b, const recip_t<r4>& rc) {
+    rpair<r4> q = mul2(a.re, rc.x, a.im, rc.x);
+    rpair<r4> t = mul2(b, q.x, b, q.y);
+    rpair<r4> d = add2(a.re, neg(t.x), a.im, neg(t.y));
+    rpair<r4> u = mul2(rc.x, d.x, rc.x, d.y);
+    rpair<r4> r = add2(q.x, u.x, q.y, u.y);
+    return {r.x, r.y};
 }
 
 // Smith division (complex.hpp:47-58); status 3 on a zero divisor.

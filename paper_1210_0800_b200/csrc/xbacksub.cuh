@@ -62,14 +62,10 @@ XB_DEVICE void store_aos(double* p, const cx<real_t<L>>& z) {
 template <int L>
 XB_DEVICE cx<real_t<L>> smith_apply(const cx<real_t<L>>& a, const smith_prep<L>& s) {
     using R = real_t<L>;
-    if (s.br) {
-        R nre = add(a.re, mul(a.im, s.t));
-        R nim = sub(a.im, mul(a.re, s.t));
-        return {divide(nre, s.d, s.rc), divide(nim, s.d, s.rc)};
-    }
-    R nre = add(mul(a.re, s.t), a.im);
-    R nim = sub(mul(a.im, s.t), a.re);
-    return {divide(nre, s.d, s.rc), divide(nim, s.d, s.rc)};
+    rpair<R> p = mul2(a.im, s.t, a.re, s.t);
+    rpair<R> nu = s.br ? add2(a.re, p.x, a.im, neg(p.y))    // a.re + a.im*t, a.im - a.re*t
+                       : add2(p.y, a.im, p.x, neg(a.re));  // a.re*t + a.im, a.im*t - a.re
+    return cdivide_real(cx<R>{nu.x, nu.y}, s.d, s.rc);
 }
 
 // CTA-wide.  r: AoS n x n (column-major), y: AoS n, xs: shared n*2L doubles,

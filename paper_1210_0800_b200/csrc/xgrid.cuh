@@ -95,6 +95,11 @@ XB_DEVICE V cta_tree(int m, int rpt, V* red, LeafFn leaf) {
     return red[kGridWarps];
 }
 
+XB_DEVICE unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 XB_DEVICE int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
             for (int i = 0; i < f.rpt; ++i) {
                 if (tid * f.rpt + i < m) {
                     C a = f.load(col, i, tid);
-                    C qv = {divide(a.re, rkk, rc), divide(a.im, rkk, rc)};
+                    C qv = cdivide_real(a, rkk, rc);
                     if (!cfinite(qv)) ok = false;
                     f.store(col, i, tid, qv);
                 }
@@ -226,6 +231,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
             }
             __threadfence();
             st_release(p.flags + j, ok ? 1 : 2);
+            if (p.trace) p.trace[j * 4 + 2] = gtimer();
         }
         return ok;
     };
@@ -255,6 +261,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
             for (int e = tid; e < f.COL; e += kGridThreads) smem[e] = __ldcg(qk + e);
         }
         __syncthreads();
+        if (p.trace && tid == 0 && j0 == k + 1) p.trace[(k + 1) * 4 + 0] = gtimer();
         const long long pos_k = 1 + (long long)k * (ncol + 1);
         for (int j = j0; j < ncol; j += G) {
             double* col = colp(j);
@@ -278,6 +285,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
                 else
                     store_aos<L>(ydst + (int64_t)k * L2, r);
             }
+            if (p.trace && tid == 0 && j == k + 1) p.trace[(k + 1) * 4 + 1] = gtimer();
             if (ok && j == k + 1 && j < n) {
                 if (!normalize_publish(j)) {
                     abort = true;
@@ -293,6 +301,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
             }
         }
         __syncthreads();
+        if (p.trace && tid == 0) atomicMax(p.trace + (k + 1) * 4 + 3, gtimer());
     }
 
     // z = column_norm(b) by its owner (mgs.hpp:155)

@@ -90,7 +90,7 @@ struct mgs_warp {
 #pragma unroll 1
         for (int t = 0; t < cnt; ++t) {
             C a = f.load(col, t, lane);
-            C q = {divide(a.re, rkk, rc), divide(a.im, rkk, rc)};
+            C q = cdivide_real(a, rkk, rc);
             ok = ok && cfinite(q);
             f.store(col, t, lane, q);
             f.store(slot, t, lane, q);

@@ -83,6 +83,7 @@ struct GridParams {
     double* norms;      // ncol * L
     int* flags;         // n: 0 pending, 1 published, 2 abort
     unsigned long long* key;  // global status key (init kNoError)
+    unsigned long long* trace;  // optional (dev): 4 globaltimer stamps per pivot
 };
 
 constexpr int kGridRowsPerThreadMax = 4;  // m <= 1024

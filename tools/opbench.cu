@@ -76,6 +76,9 @@ __global__ void __launch_bounds__(128) bench(double* sink, int reps) {
                 if (OP == 2) x[c] = cmul(x[c], w);
                 if (OP == 3) x[c] = cadd(x[c], (t & 1) ? cx<R>{neg(w.re), neg(w.im)} : w);
                 if (OP == 4) x[c] = csub(x[c], cmul(w, y[(t + c + 1) & 3]));
+                // zero-limb operands (widened constants): the general paths
+                if (OP == 5) x[c].re = add(x[c].re, rmake<R>((t & 1) ? -1.0 : 1.0));
+                if (OP == 6) x[c].re = mul(x[c].re, rmake<R>((t & 1) ? 0.75 : 1.3125));
             }
         }
     }
@@ -106,6 +109,23 @@ void run(const char* name, double fp64_per_op, int blocks_per_sm, int sms, doubl
            cudaGetErrorString(cudaGetLastError()));
 }
 
+// latency: one warp, one dependent chain; ns per op
+template <class R, int OP>
+void lat(const char* name, double* sink) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    bench<R, OP, 1><<<1, 32>>>(sink, 1);
+    cudaEventRecord(e0);
+    bench<R, OP, 1><<<1, 32>>>(sink, 16);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ns = ms * 1e6 / (16.0 * K);
+    printf("latency %-10s %8.1f ns/op  (%6.0f cycles at 1.965 GHz)\n", name, ns, ns * 1.965);
+}
+
 int main() {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -113,6 +133,15 @@ int main() {
     cudaMalloc(&sink, sizeof(double) * 148 * 64 * 128);
     // reference per-op FP64 instruction weights (Appendix B): qd add 90, mul 179,
     // cmul 896, cadd 180; dd add 20, mul 9, cmul 76, cadd 40
+    lat<r4, 0>("qd add", sink);
+    lat<r4, 1>("qd mul", sink);
+    lat<r4, 2>("qd cmul", sink);
+    lat<r4, 3>("qd cadd", sink);
+    lat<r4, 4>("qd axpy", sink);
+    lat<r4, 5>("qd add0", sink);
+    lat<r4, 6>("qd mul0", sink);
+    lat<r2, 0>("dd add", sink);
+    lat<r2, 1>("dd mul", sink);
     for (int bps : {4, 8}) {
         run<r4, 0, 1>("qd add", 90, bps, sms, sink);
         run<r4, 0, 2>("qd add", 90, bps, sms, sink);
