@@ -113,13 +113,21 @@ int check_shape(xqr_ctx* ctx, xqr_status* st, int limbs, int64_t batch, int64_t 
     return 0;
 }
 
-// A single system large enough to feed several SMs goes to the persistent
-// grid kernel (xgrid.cuh); small ones stay on one CTA (xmgs.cuh).
+// A single system large enough to feed several SMs goes to the cluster grid
+// kernel (xgrid2.cuh); small ones stay on one CTA (xmgs.cuh).
 bool use_grid_path(xqr_ctx* ctx, int m, int n) {
     if (const char* e = std::getenv("XQR_FORCE_CTA")) {
         if (e[0] == '1') return false;
     }
-    return ctx->coop && n >= 8 && m <= 256 * xb::kGridRowsPerThreadMax;
+    return ctx->coop && n >= 8 && m >= 64 && m <= xb::kGridMaxRows;
+}
+
+size_t grid_scratch_bytes(bool lsq, int limbs, int m, int n) {
+    const int ncol = n + (lsq ? 1 : 0);
+    return sizeof(double) * ((size_t)ncol * m * 2 * limbs + (lsq ? xb::rws_doubles(limbs, n) : 0) +
+                             (size_t)ncol * limbs) +
+           sizeof(int) * ((size_t)n + 4) + sizeof(unsigned long long) * (8 * (size_t)(n + 1) + 1) +
+           8 * 256;
 }
 
 int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_a,
@@ -129,7 +137,7 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     xb::GridParams p{};
     p.m = m;
     p.n = n;
-    p.rpt = xb::rows_per_thread(m);
+    xb::grid_shape(m, p.cs, p.rpt);
     p.a = d_a;
     p.b = d_b;
     p.q = d_q;
@@ -138,43 +146,45 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     p.z = d_z;
     p.st = d_st;
     arena_plan plan;
-    const size_t o_ws = plan.add(sizeof(double) * (size_t)ncol * 2 * limbs * 256 * p.rpt);
+    const size_t o_ws = plan.add(sizeof(double) * (size_t)ncol * m * 2 * limbs);
     const size_t o_rws = plan.add(lsq ? sizeof(double) * xb::rws_doubles(limbs, n) : 0);
     const size_t o_nrm = plan.add(sizeof(double) * (size_t)ncol * limbs);
-    const size_t o_flg = plan.add(sizeof(int) * (size_t)n);
+    const size_t o_flg = plan.add(sizeof(int) * ((size_t)n + 4));
     const size_t o_key = plan.add(sizeof(unsigned long long));
     const char* trace_path = std::getenv("XQR_GRID_TRACE");  // dev instrumentation
-    const size_t o_trc = plan.add(trace_path ? sizeof(unsigned long long) * 4 * (size_t)(n + 1) : 0);
+    const size_t o_trc = plan.add(trace_path ? sizeof(unsigned long long) * 8 * (size_t)(n + 1) : 0);
     cudaError_t e = ensure_arena(ctx, scratch_off + plan.total + 256);
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
     p.ws = reinterpret_cast<double*>(at(ctx, scratch_off + o_ws));
     p.rws = lsq ? reinterpret_cast<double*>(at(ctx, scratch_off + o_rws)) : nullptr;
     p.norms = reinterpret_cast<double*>(at(ctx, scratch_off + o_nrm));
     p.flags = reinterpret_cast<int*>(at(ctx, scratch_off + o_flg));
+    p.counters = p.flags + n;
     p.key = reinterpret_cast<unsigned long long*>(at(ctx, scratch_off + o_key));
     p.trace = trace_path ? reinterpret_cast<unsigned long long*>(at(ctx, scratch_off + o_trc)) : nullptr;
-    if (p.trace) cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * 4 * (size_t)(n + 1), ctx->stream);
-    cudaMemsetAsync(p.flags, 0, sizeof(int) * (size_t)n, ctx->stream);
+    cudaMemsetAsync(p.flags, 0, sizeof(int) * ((size_t)n + 4), ctx->stream);
     cudaMemsetAsync(p.key, 0xFF, sizeof(unsigned long long), ctx->stream);
-    const int grid = std::min(ncol, ctx->num_sms);
+    if (p.trace) cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * 8 * (size_t)(n + 1), ctx->stream);
+    const int max_clusters = ctx->num_sms / p.cs;
     if (timed) cudaEventRecord(ctx->ev0, ctx->stream);
     switch (limbs) {
-        case 1: e = xb::launch_grid_L1(p, grid, lsq, ctx->stream); break;
-        case 2: e = xb::launch_grid_L2(p, grid, lsq, ctx->stream); break;
-        default: e = xb::launch_grid_L4(p, grid, lsq, ctx->stream); break;
+        case 1: e = xb::launch_grid_L1(p, max_clusters, lsq, ctx->stream); break;
+        case 2: e = xb::launch_grid_L2(p, max_clusters, lsq, ctx->stream); break;
+        default: e = xb::launch_grid_L4(p, max_clusters, lsq, ctx->stream); break;
     }
     if (timed) cudaEventRecord(ctx->ev1, ctx->stream);
     ctx->timed = timed;
     ctx->launches += 1;
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "grid kernel launch");
     if (p.trace) {
-        std::vector<unsigned long long> h(4 * (size_t)(n + 1));
+        std::vector<unsigned long long> h(8 * (size_t)(n + 1));
         cudaMemcpyAsync(h.data(), p.trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
                         ctx->stream);
         cudaStreamSynchronize(ctx->stream);
         if (FILE* fp = std::fopen(trace_path, "w")) {
             for (int j = 0; j <= n; ++j)
-                std::fprintf(fp, "%d %llu %llu %llu %llu\n", j, h[4 * j], h[4 * j + 1], h[4 * j + 2], h[4 * j + 3]);
+                std::fprintf(fp, "%d %llu %llu %llu %llu %llu %llu %llu %llu\n", j, h[8 * j], h[8 * j + 1],
+                             h[8 * j + 2], h[8 * j + 3], h[8 * j + 4], h[8 * j + 5], h[8 * j + 6], h[8 * j + 7]);
             std::fclose(fp);
         }
     }
@@ -362,11 +372,7 @@ static int solve_host(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t 
     const int ncol = (int)n + (lsq ? 1 : 0);
     size_t scratch = sizeof(double) * (size_t)batch *
                      (xb::ws_doubles(limbs, (int)m, ncol) + (lsq ? xb::rws_doubles(limbs, (int)n) : 0));
-    if (batch == 1)  // grid path: rows padded to 256*rpt, plus norms / flags / key
-        scratch = std::max(scratch, sizeof(double) * ((size_t)ncol * 2 * limbs * 256 *
-                                                          xb::rows_per_thread((int)m) +
-                                                      (lsq ? xb::rws_doubles(limbs, (int)n) : 0) +
-                                                      (size_t)ncol * limbs + n) + 4096);
+    if (batch == 1) scratch = std::max(scratch, grid_scratch_bytes(lsq, limbs, (int)m, (int)n));
     cudaError_t e = ensure_arena(ctx, plan.total + scratch + 512);
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
     // stage inputs through pinned memory

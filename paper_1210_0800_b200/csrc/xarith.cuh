@@ -368,7 +368,7 @@ inline long g_add_general = 0, g_mul_general = 0, g_add_zt = 0;
 #else
 #define XB_COUNT(c) ((void)0)
 #endif
-XB_GEN r4 add_general(const r4& a, const r4& b) {
+XB_GEN r4 add_general(const r4 a, const r4 b) {
     XB_COUNT(g_add_general);
     int i = 0, j = 0, k = 0;
     double u, v;
@@ -478,6 +478,17 @@ XB_DEV void renorm4_fast(double& c0, double& c1, double& c2, double& c3, bool& o
     c3 = u3;
 }
 
+// The reference branch trees as calls: the fast forms fall back to them on the
+// same pre-renormalisation components (no recomputation).
+XB_GEN r4 renorm4_general(double c0, double c1, double c2, double c3) {
+    renorm4(c0, c1, c2, c3);
+    return {c0, c1, c2, c3};
+}
+XB_GEN r4 renorm5_general(double c0, double c1, double c2, double c3, double c4) {
+    renorm5(c0, c1, c2, c3, c4);
+    return {c0, c1, c2, c3};
+}
+
 // renorm (five components, quad_double.hpp:78-154), common case likewise:
 // every zero test of the reference tree takes its "non-zero" side.
 XB_DEV void renorm5_fast(double& c0, double& c1, double& c2, double& c3, double c4, bool& ok) {
@@ -515,92 +526,225 @@ XB_DEV void renorm5_fast(double& c0, double& c1, double& c2, double& c3, double 
 // warp only when some lane needs it.  add_fast() reports whether its result
 // is the reference's (ok); callers with independent adds run all fast paths
 // first and branch once.
-XB_DEV r4 add_fast(const r4& a, const r4& b, bool& okr) {
+// The level-paired fast path in three stages (setup, six merge steps,
+// finish), so that independent adds can be written in lockstep (add_fast2)
+// and their dependency chains interleave.
+struct qadd_st {
+    double m2, m3, m4, m5, m6, m7;
+    double u, v, x0, x1, x2, x3;
+    int k;
+    bool ok;
+};
+XB_DEV void qadd_setup(const r4& a, const r4& b, qadd_st& q) {
     const bool f0 = dabs(a.c0) > dabs(b.c0), f1 = dabs(a.c1) > dabs(b.c1);
     const bool f2 = dabs(a.c2) > dabs(b.c2), f3 = dabs(a.c3) > dabs(b.c3);
     const double m0 = f0 ? a.c0 : b.c0, m1 = f0 ? b.c0 : a.c0;
-    const double m2 = f1 ? a.c1 : b.c1, m3 = f1 ? b.c1 : a.c1;
-    const double m4 = f2 ? a.c2 : b.c2, m5 = f2 ? b.c2 : a.c2;
-    const double m6 = f3 ? a.c3 : b.c3, m7 = f3 ? b.c3 : a.c3;
+    q.m2 = f1 ? a.c1 : b.c1;
+    q.m3 = f1 ? b.c1 : a.c1;
+    q.m4 = f2 ? a.c2 : b.c2;
+    q.m5 = f2 ? b.c2 : a.c2;
+    q.m6 = f3 ? a.c3 : b.c3;
+    q.m7 = f3 ? b.c3 : a.c3;
     // the smaller limb of level l beats both limbs of level l+1 strictly: then
     // the reference's comparison against the successor of the taken limb
     // picks it (|a_{l+1}| > |b_l| is false, resp. |a_l| > |b_{l+1}| is true)
-    bool ok = (dabs(m1) > dabs(m2)) && (dabs(m3) > dabs(m4)) && (dabs(m5) > dabs(m6));
-    double u, v;
-    quick_two_sum(m0, m1, u, v);
-    double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
-    int k = 0;
-    qadd_step<0>(u, v, m2, k, x0, x1, x2, x3);
-    qadd_step<1>(u, v, m3, k, x0, x1, x2, x3);
-    qadd_step<2>(u, v, m4, k, x0, x1, x2, x3);
-    qadd_step<3>(u, v, m5, k, x0, x1, x2, x3);
-    qadd_step<3>(u, v, m6, k, x0, x1, x2, x3);
-    ok = ok && (k <= 3);
-    qadd_step<3>(u, v, m7, k, x0, x1, x2, x3);
-    // loop exit with everything consumed: x[k] = u; if (k < 3) x[k + 1] = v
-    x0 = (k == 0) ? u : x0;
-    x1 = (k == 1) ? u : ((k == 0) ? v : x1);
-    x2 = (k == 2) ? u : ((k == 1) ? v : x2);
-    x3 = (k == 3) ? u : ((k == 2) ? v : x3);
-    bool okn;
-    renorm4_fast(x0, x1, x2, x3, okn);
-    okr = ok && okn;
-    return {x0, x1, x2, x3};
+    q.ok = (dabs(m1) > dabs(q.m2)) && (dabs(q.m3) > dabs(q.m4)) && (dabs(q.m5) > dabs(q.m6));
+    quick_two_sum(m0, m1, q.u, q.v);
+    q.x0 = q.x1 = q.x2 = q.x3 = 0.0;
+    q.k = 0;
 }
-// Second fast path, for an operand whose three lower limbs are zero (a
-// double widened to quad-double: the constants and seeds of the Newton
-// iterations, the generator's widened inputs).  The reference merge then
-// takes the two heads, the other operand's lower limbs, and the zeros last:
-//   a = (x,0,0,0): heads, b1, b2, b3, a1, a2, a3  (a0 taken second needs
-//                  |a0| > |b1|)
-//   b = (y,0,0,0): heads, a1, a2, a3, b1, b2, b3  (needs |a1|, |a2|, |a3| > 0,
-//                  and a0 taken first needs !(|a1| > |b0|), second |a0| > 0)
-// again exactly the comparisons the reference makes.
-XB_DEV r4 add_zt_fast(const r4& a, const r4& b, bool& okr) {
-    const bool f0 = dabs(a.c0) > dabs(b.c0);
+template <int STEP>
+XB_DEV void qadd_run(qadd_st& q) {
+    const double s = STEP == 0 ? q.m2 : STEP == 1 ? q.m3 : STEP == 2 ? q.m4 : STEP == 3 ? q.m5
+                   : STEP == 4 ? q.m6 : q.m7;
+    if (STEP == 5) q.ok = q.ok && (q.k <= 3);  // the loop reaches its last step
+    qadd_step<(STEP < 3 ? STEP : 3)>(q.u, q.v, s, q.k, q.x0, q.x1, q.x2, q.x3);
+}
+XB_DEV r4 qadd_finish(qadd_st& q, bool& okr) {
+    // loop exit with everything consumed: x[k] = u; if (k < 3) x[k + 1] = v
+    const int k = q.k;
+    const double x0 = (k == 0) ? q.u : q.x0;
+    const double x1 = (k == 1) ? q.u : ((k == 0) ? q.v : q.x1);
+    const double x2 = (k == 2) ? q.u : ((k == 1) ? q.v : q.x2);
+    const double x3 = (k == 3) ? q.u : ((k == 2) ? q.v : q.x3);
+    double y0 = x0, y1 = x1, y2 = x2, y3 = x3;
+    bool okn;
+    renorm4_fast(y0, y1, y2, y3, okn);
+    okr = q.ok;
+    if (!okn) return renorm4_general(x0, x1, x2, x3);
+    return {y0, y1, y2, y3};
+}
+XB_DEV r4 add_fast(const r4& a, const r4& b, bool& okr) {
+    qadd_st q;
+    qadd_setup(a, b, q);
+    qadd_run<0>(q);
+    qadd_run<1>(q);
+    qadd_run<2>(q);
+    qadd_run<3>(q);
+    qadd_run<4>(q);
+    qadd_run<5>(q);
+    return qadd_finish(q, okr);
+}
+// two independent adds in lockstep
+XB_DEV void add_fast2(const r4& a1, const r4& b1, const r4& a2, const r4& b2, r4& o1, bool& k1,
+                      r4& o2, bool& k2) {
+    qadd_st p, q;
+    qadd_setup(a1, b1, p);
+    qadd_setup(a2, b2, q);
+    qadd_run<0>(p);
+    qadd_run<0>(q);
+    qadd_run<1>(p);
+    qadd_run<1>(q);
+    qadd_run<2>(p);
+    qadd_run<2>(q);
+    qadd_run<3>(p);
+    qadd_run<3>(q);
+    qadd_run<4>(p);
+    qadd_run<4>(q);
+    qadd_run<5>(p);
+    qadd_run<5>(q);
+    o1 = qadd_finish(p, k1);
+    o2 = qadd_finish(q, k2);
+}
+// Second fast path for merges that are not level-paired but still fixed:
+//   a = (x,0,0,0):  heads, b1, b2, b3, a1, a2, a3  (b0 taken first needs
+//                   |a0| > |b1|)                      -- widened constants,
+//   b = (y,0,0,0):  heads, a1, a2, a3, b1, b2, b3  (needs |a1|,|a2|,|a3| > 0
+//                   and a0 taken first !(|a1| > |b0|), b0 first |a0| > 0),
+//   disjoint:       a0..a3 then b0..b3 (every |a_i| > |b0|), or b0..b3 then
+//                   a0..a3 (no |a0| > |b_j|)          -- a tiny Newton
+//                   correction, a zero operand.
+// Each pattern is recognised by exactly the comparisons the reference merge
+// makes; the merge steps are then the same six fixed steps.
+XB_DEV r4 add_alt_fast(const r4& a, const r4& b, bool& okr) {
+    const double A0 = dabs(a.c0), A1 = dabs(a.c1), A2 = dabs(a.c2), A3 = dabs(a.c3);
+    const double B0 = dabs(b.c0), B1 = dabs(b.c1), B2 = dabs(b.c2), B3 = dabs(b.c3);
+    const bool f0 = A0 > B0;
+    const bool da = f0 && (A1 > B0) && (A2 > B0) && (A3 > B0);              // a first
+    const bool db = !f0 && !(A0 > B1) && !(A0 > B2) && !(A0 > B3);          // b first
     const bool ta = (a.c1 == 0.0) && (a.c2 == 0.0) && (a.c3 == 0.0);
     const bool tb = (b.c1 == 0.0) && (b.c2 == 0.0) && (b.c3 == 0.0);
-    bool ok;
-    if (ta) {
-        ok = f0 || (dabs(a.c0) > dabs(b.c1));
+    const bool pa = ta && (f0 || (A0 > B1));
+    const bool pb = tb && (A1 > 0.0) && (A2 > 0.0) && (A3 > 0.0) && (f0 ? !(A1 > B0) : (A0 > 0.0));
+    qadd_st q;
+    double m0, m1;
+    if (da || db) {
+        const r4& h = da ? a : b;
+        const r4& l = da ? b : a;
+        m0 = h.c0;
+        m1 = h.c1;
+        q.m2 = h.c2;
+        q.m3 = h.c3;
+        q.m4 = l.c0;
+        q.m5 = l.c1;
+        q.m6 = l.c2;
+        q.m7 = l.c3;
     } else {
-        ok = tb && (dabs(a.c1) > 0.0) && (dabs(a.c2) > 0.0) && (dabs(a.c3) > 0.0) &&
-             (f0 ? !(dabs(a.c1) > dabs(b.c0)) : (dabs(a.c0) > 0.0));
+        m0 = f0 ? a.c0 : b.c0;
+        m1 = f0 ? b.c0 : a.c0;
+        q.m2 = pa ? b.c1 : a.c1;
+        q.m3 = pa ? b.c2 : a.c2;
+        q.m4 = pa ? b.c3 : a.c3;
+        q.m5 = pa ? a.c1 : b.c1;
+        q.m6 = pa ? a.c2 : b.c2;
+        q.m7 = pa ? a.c3 : b.c3;
     }
-    const double m0 = f0 ? a.c0 : b.c0, m1 = f0 ? b.c0 : a.c0;
-    const double m2 = ta ? b.c1 : a.c1, m3 = ta ? b.c2 : a.c2, m4 = ta ? b.c3 : a.c3;
-    const double m5 = ta ? a.c1 : b.c1, m6 = ta ? a.c2 : b.c2, m7 = ta ? a.c3 : b.c3;
-    double u, v;
-    quick_two_sum(m0, m1, u, v);
+    q.ok = da || db || pa || pb;
+    quick_two_sum(m0, m1, q.u, q.v);
+    q.x0 = q.x1 = q.x2 = q.x3 = 0.0;
+    q.k = 0;
+    qadd_run<0>(q);
+    qadd_run<1>(q);
+    qadd_run<2>(q);
+    qadd_run<3>(q);
+    qadd_run<4>(q);
+    qadd_run<5>(q);
+    return qadd_finish(q, okr);
+}
+
+// The reference merge in full generality, but predicated instead of
+// branched (quad_double.hpp:216-257): the heads are picked by register
+// selects on the consumed counts i, j; the six loop steps always execute,
+// and after the loop has exited (k == 4) they change nothing; the leftover
+// fold adds a's then b's remaining limbs in order.  Same operations on the
+// same operands as the reference for every input; no lane divergence.
+XB_DEV double pick4v(int i, const r4& a) {
+    const double lo = (i & 1) ? a.c1 : a.c0;
+    const double hi = (i & 1) ? a.c3 : a.c2;
+    return (i & 2) ? hi : lo;
+}
+XB_DEV r4 add_merge_pred(const r4& a, const r4& b) {
+    int i = 0, j = 0;
+    bool t = dabs(a.c0) > dabs(b.c0);
+    double u = t ? a.c0 : b.c0;
+    i += t ? 1 : 0;
+    j += t ? 0 : 1;
+    double ai = t ? a.c1 : a.c0, bj = t ? b.c0 : b.c1;
+    t = dabs(ai) > dabs(bj);
+    double v = t ? ai : bj;
+    i += t ? 1 : 0;
+    j += t ? 0 : 1;
+    quick_two_sum(u, v, u, v);
     double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
     int k = 0;
-    qadd_step<0>(u, v, m2, k, x0, x1, x2, x3);
-    qadd_step<1>(u, v, m3, k, x0, x1, x2, x3);
-    qadd_step<2>(u, v, m4, k, x0, x1, x2, x3);
-    qadd_step<3>(u, v, m5, k, x0, x1, x2, x3);
-    qadd_step<3>(u, v, m6, k, x0, x1, x2, x3);
-    ok = ok && (k <= 3);
-    qadd_step<3>(u, v, m7, k, x0, x1, x2, x3);
+#pragma unroll
+    for (int step = 0; step < 6; ++step) {
+        const bool live = (k < 4);
+        ai = pick4v(i, a);
+        bj = pick4v(j, b);
+        const bool ta = (j >= 4) || (i < 4 && dabs(ai) > dabs(bj));
+        const double s = ta ? ai : bj;
+        double tt, te, uu, ue;
+        two_sum(v, s, tt, te);
+        two_sum(u, tt, uu, ue);
+        const bool zb = (te != 0.0);
+        const bool emit = live && (ue != 0.0) && zb;
+        v = live ? (zb ? te : ue) : v;
+        u = live ? (emit ? ue : uu) : u;
+        x0 = (emit && k == 0) ? uu : x0;
+        x1 = (emit && k == 1) ? uu : x1;
+        x2 = (emit && k == 2) ? uu : x2;
+        x3 = (emit && k == 3) ? uu : x3;
+        k += emit ? 1 : 0;
+        i += (live && ta) ? 1 : 0;
+        j += (live && !ta) ? 1 : 0;
+    }
+    // exhausted with k < 4: x[k] = u; if (k < 3) x[k + 1] = v
     x0 = (k == 0) ? u : x0;
     x1 = (k == 1) ? u : ((k == 0) ? v : x1);
     x2 = (k == 2) ? u : ((k == 1) ? v : x2);
     x3 = (k == 3) ? u : ((k == 2) ? v : x3);
+    // leftovers (only after an early exit): a's first, then b's
+    if (i <= 0) x3 = dadd(x3, a.c0);
+    if (i <= 1) x3 = dadd(x3, a.c1);
+    if (i <= 2) x3 = dadd(x3, a.c2);
+    if (i <= 3) x3 = dadd(x3, a.c3);
+    if (j <= 0) x3 = dadd(x3, b.c0);
+    if (j <= 1) x3 = dadd(x3, b.c1);
+    if (j <= 2) x3 = dadd(x3, b.c2);
+    if (j <= 3) x3 = dadd(x3, b.c3);
+    double y0 = x0, y1 = x1, y2 = x2, y3 = x3;
     bool okn;
-    renorm4_fast(x0, x1, x2, x3, okn);
-    okr = ok && okn;
-    return {x0, x1, x2, x3};
+    renorm4_fast(y0, y1, y2, y3, okn);
+    if (!okn) return renorm4_general(x0, x1, x2, x3);
+    return {y0, y1, y2, y3};
 }
 
-// Everything the fast paths do not cover: the zero-tail path, else the
-// reference merge (one call, so the inlined fast path stays small).
-XB_GEN r4 add_slow(const r4& a, const r4& b) {
+// Everything the level-paired path does not cover: the alternative fixed
+// merges, else the reference merge (one call, so the inlined fast path stays
+// small).
+XB_GEN r4 add_slow(const r4 a, const r4 b) {
+#if defined(XB_ADD_SLOW_BRANCHY)
     bool ok;
-    r4 r = add_zt_fast(a, b, ok);
+    r4 r = add_alt_fast(a, b, ok);
     if (!ok) r = add_general(a, b);
     return r;
+#else
+    return add_merge_pred(a, b);
+#endif
 }
 
-XB_OP4 r4 add(const r4& a, const r4& b) {
+XB_OP4 r4 add(const r4 a, const r4 b) {
     bool ok;
     r4 r = add_fast(a, b, ok);
     if (!ok) r = add_slow(a, b);
@@ -679,20 +823,45 @@ XB_DEV void qmul_core(const r4& a, const r4& b, double& p0, double& p1, double& 
     t1c = dadd(t1c, w);
 
 }
+XB_DEV r4 qmul_finish(double p0, double p1, double s0, double t0c, double t1c) {
+    double y0 = p0, y1 = p1, y2 = s0, y3 = t0c;
+    bool okn;
+    renorm5_fast(y0, y1, y2, y3, t1c, okn);
+    if (!okn) return renorm5_general(p0, p1, s0, t0c, t1c);
+    return {y0, y1, y2, y3};
+}
 XB_DEV r4 mul_fast(const r4& a, const r4& b, bool& ok) {
     double p0, p1, s0, t0c, t1c;
     qmul_core(a, b, p0, p1, s0, t0c, t1c);
-    renorm5_fast(p0, p1, s0, t0c, t1c, ok);
-    return {p0, p1, s0, t0c};
+    ok = true;
+    return qmul_finish(p0, p1, s0, t0c, t1c);
 }
-XB_GEN r4 mul_general(const r4& a, const r4& b) {
+// independent products in lockstep: the cores first, then the renormalisations
+XB_DEV void mul_fast2(const r4& a1, const r4& b1, const r4& a2, const r4& b2, r4& o1, bool& k1,
+                      r4& o2, bool& k2) {
+    double p0, p1, s0, t0c, t1c, q0, q1, u0, v0c, v1c;
+    qmul_core(a1, b1, p0, p1, s0, t0c, t1c);
+    qmul_core(a2, b2, q0, q1, u0, v0c, v1c);
+    double y0 = p0, y1 = p1, y2 = s0, y3 = t0c, w0 = q0, w1 = q1, w2 = u0, w3 = v0c;
+    bool n1, n2;
+    renorm5_fast(y0, y1, y2, y3, t1c, n1);
+    renorm5_fast(w0, w1, w2, w3, v1c, n2);
+    o1 = {y0, y1, y2, y3};
+    o2 = {w0, w1, w2, w3};
+    if (!(n1 && n2)) {
+        if (!n1) o1 = renorm5_general(p0, p1, s0, t0c, t1c);
+        if (!n2) o2 = renorm5_general(q0, q1, u0, v0c, v1c);
+    }
+    k1 = k2 = true;
+}
+XB_GEN r4 mul_general(const r4 a, const r4 b) {
     XB_COUNT(g_mul_general);
     double p0, p1, s0, t0c, t1c;
     qmul_core(a, b, p0, p1, s0, t0c, t1c);
     renorm5(p0, p1, s0, t0c, t1c);
     return {p0, p1, s0, t0c};
 }
-XB_OP4 r4 mul(const r4& a, const r4& b) {
+XB_OP4 r4 mul(const r4 a, const r4 b) {
     bool ok;
     r4 r = mul_fast(a, b, ok);
     if (!ok) r = mul_general(a, b);
@@ -703,7 +872,7 @@ XB_DEV r4 mul_pwr2(const r4& a, double p2) {  // :341-343
     return {dmul(a.c0, p2), dmul(a.c1, p2), dmul(a.c2, p2), dmul(a.c3, p2)};
 }
 // quad_double.hpp:359-370
-XB_OP2 r4 rsqrt_ref(const r4& a) {
+XB_OP2 r4 rsqrt_ref(const r4 a) {
     if (a.c0 == 0.0 && a.c1 == 0.0 && a.c2 == 0.0 && a.c3 == 0.0) return {0.0, 0.0, 0.0, 0.0};
     r4 x = make4(ddiv(1.0, dsqrt(a.c0)));
 #pragma unroll 1
@@ -773,7 +942,7 @@ XB_DEV r2 divide(const r2& a, const r2& b, const recip_t<r2>& rc) {
     return add(q, mul(r, rc.x1));
 }
 
-XB_OP2 recip_t<r4> recip(const r4& b, int& status) {
+XB_OP2 recip_t<r4> recip(const r4 b, int& status) {
     if (b.c0 == 0.0) {
         status = 3;
         return {{0.0, 0.0, 0.0, 0.0}};
@@ -824,7 +993,8 @@ XB_DEV rpair<R> mul2(const R& a1, const R& b1, const R& a2, const R& b2) {
 template <>
 XB_DEV rpair<r4> add2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2) {
     bool k1, k2;
-    rpair<r4> o{add_fast(a1, b1, k1), add_fast(a2, b2, k2)};
+    rpair<r4> o;
+    add_fast2(a1, b1, a2, b2, o.x, k1, o.y, k2);
     if (!(k1 && k2)) {
         if (!k1) o.x = add_slow(a1, b1);
         if (!k2) o.y = add_slow(a2, b2);
@@ -834,7 +1004,8 @@ XB_DEV rpair<r4> add2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2
 template <>
 XB_DEV rpair<r4> mul2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2) {
     bool k1, k2;
-    rpair<r4> o{mul_fast(a1, b1, k1), mul_fast(a2, b2, k2)};
+    rpair<r4> o;
+    mul_fast2(a1, b1, a2, b2, o.x, k1, o.y, k2);
     if (!(k1 && k2)) {
         if (!k1) o.x = mul_general(a1, b1);
         if (!k2) o.y = mul_general(a2, b2);
@@ -866,6 +1037,24 @@ XB_DEV cx<R> cmul_t(const cx<R>& a, const cx<R>& b) {
     rpair<R> o = add2(p.x, neg(p.y), q.x, q.y);
     return {o.x, o.y};
 }
+#if !(XB_CALLS & 4)
+// quad-double: all four products' fast paths, one branch, then the sums
+template <>
+XB_DEV cx<r4> cmul_t<r4>(const cx<r4>& a, const cx<r4>& b) {
+    r4 p1, p2, p3, p4;
+    bool k1, k2, k3, k4;
+    mul_fast2(a.re, b.re, a.im, b.im, p1, k1, p2, k2);
+    mul_fast2(a.re, b.im, a.im, b.re, p3, k3, p4, k4);
+    if (!(k1 && k2 && k3 && k4)) {
+        if (!k1) p1 = mul_general(a.re, b.re);
+        if (!k2) p2 = mul_general(a.im, b.im);
+        if (!k3) p3 = mul_general(a.re, b.im);
+        if (!k4) p4 = mul_general(a.im, b.re);
+    }
+    rpair<r4> o = add2(p1, neg(p2), p3, p4);
+    return {o.x, o.y};
+}
+#endif
 template <class R>
 XB_DEV cx<R> cadd(const cx<R>& a, const cx<R>& b) {
     return cadd_t(a, b);
@@ -875,18 +1064,18 @@ XB_DEV cx<R> cmul(const cx<R>& a, const cx<R>& b) {
     return cmul_t(a, b);
 }
 // quad-double: overloads (preferred over the templates) that can be calls
-XB_OP2 cx<r4> cadd(const cx<r4>& a, const cx<r4>& b) { return cadd_t(a, b); }
-XB_OP2 cx<r4> cmul(const cx<r4>& a, const cx<r4>& b) { return cmul_t(a, b); }
+XB_OP2 cx<r4> cadd(const cx<r4> a, const cx<r4> b) { return cadd_t(a, b); }
+XB_OP2 cx<r4> cmul(const cx<r4> a, const cx<r4> b) { return cmul_t(a, b); }
 template <class R>
 XB_DEV cx<R> csub_t(const cx<R>& a, const cx<R>& b);
-XB_OP2 cx<r4> csub(const cx<r4>& a, const cx<r4>& b) { return csub_t(a, b); }
+XB_OP2 cx<r4> csub(const cx<r4> a, const cx<r4> b) { return csub_t(a, b); }
 // Re(conj(a) * b): the real half of cmul(cconj(a), b), same ops.
 template <class R>
 XB_DEV R cdot_re(const cx<R>& a, const cx<R>& b) {
     rpair<R> p = mul2(a.re, b.re, neg(a.im), b.im);
     return sub(p.x, p.y);
 }
-XB_OP2 r4 cdot_re(const cx<r4>& a, const cx<r4>& b) {
+XB_OP2 r4 cdot_re(const cx<r4> a, const cx<r4> b) {
     rpair<r4> p = mul2(a.re, b.re, neg(a.im), b.im);
     return sub(p.x, p.y);
 }
@@ -898,7 +1087,7 @@ XB_DEV cx<R> cdivide_real(const cx<R>& a, const R& b, const recip_t<R>& rc) {
 }
 // quad-double: q = a*x; q = q + x*(a - b*q) (quad_double.hpp:352-353) for
 // both parts in lockstep
-XB_OP2 cx<r4> cdivide_real(const cx<r4>& a, const r4& b, const recip_t<r4>& rc) {
+XB_OP2 cx<r4> cdivide_real(const cx<r4> a, const r4 b, const recip_t<r4> rc) {
     rpair<r4> q = mul2(a.re, rc.x, a.im, rc.x);
     rpair<r4> t = mul2(b, q.x, b, q.y);
     rpair<r4> d = add2(a.re, neg(t.x), a.im, neg(t.y));

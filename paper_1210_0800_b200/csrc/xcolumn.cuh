@@ -73,6 +73,21 @@ XB_DEVICE r4 shfl_idx_r<r4>(const r4& v, int s) {
             __shfl_sync(0xffffffffu, v.c2, s), __shfl_sync(0xffffffffu, v.c3, s)};
 }
 template <class R>
+XB_DEVICE R shfl_xor_r(const R& v, int m);
+template <>
+XB_DEVICE r1 shfl_xor_r<r1>(const r1& v, int m) {
+    return {__shfl_xor_sync(0xffffffffu, v.c0, m)};
+}
+template <>
+XB_DEVICE r2 shfl_xor_r<r2>(const r2& v, int m) {
+    return {__shfl_xor_sync(0xffffffffu, v.c0, m), __shfl_xor_sync(0xffffffffu, v.c1, m)};
+}
+template <>
+XB_DEVICE r4 shfl_xor_r<r4>(const r4& v, int m) {
+    return {__shfl_xor_sync(0xffffffffu, v.c0, m), __shfl_xor_sync(0xffffffffu, v.c1, m),
+            __shfl_xor_sync(0xffffffffu, v.c2, m), __shfl_xor_sync(0xffffffffu, v.c3, m)};
+}
+template <class R>
 XB_DEVICE cx<R> shfl_down_c(const cx<R>& v, int o) {
     return {shfl_down_r(v.re, o), shfl_down_r(v.im, o)};
 }

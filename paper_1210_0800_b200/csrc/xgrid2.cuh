@@ -1,0 +1,467 @@
+// xgrid2.cuh -- single-system MGS QR / least squares over the whole GPU,
+// latency-first layout (configs 2-4: cdd/cqd 256x256, cqd 512x256).
+//
+// What bounds one large system is the per-pivot dependency chain
+//   rp(k, k+1) -> |a_{k+1}|^2 tree -> sqrt -> reciprocal -> divide -> publish,
+// and inside it the latency of one quad-double operation, which is set by the
+// FP64 issue of ONE warp on its SM sub-partition (a warp FP64 instruction
+// occupies the 16-lane pipe for 2 cycles).  So the layout minimises the
+// quad-double work per lane on that chain:
+//   * a LANE PAIR owns a row: the even lane computes the real part, the odd
+//     lane the imaginary part of every complex quantity (the two halves of a
+//     complex multiply / add / divide are independent -- complex.hpp:26-65);
+//   * a column belongs to a thread-block CLUSTER of CS CTAs (CS = 4 for
+//     m = 256): 4 warps per CTA, one per SM sub-partition, 16 rows per warp;
+//   * the fixed reduction tree (reduction.hpp:34-40) runs in-lane (rows of a
+//     pair), then over lane pairs by shuffles, then over the cluster's warp
+//     partials read through distributed shared memory -- the same pairing as
+//     the sequential tree_reduce, since rows are laid out consecutively;
+//   * every warp computes the pivot's sqrt / reciprocal redundantly (no
+//     broadcast hop), then each lane divides its own half of its row.
+// Columns are distributed cyclically over clusters (column j -> cluster
+// j mod G); q_k is the finished column itself in the (AoS) workspace,
+// published with a release counter and acquired by every other cluster; the
+// owner of column k+1 updates and normalises it first (look-ahead).  The
+// working copy uses the reference's own memory image (column-major, row =
+// re limbs then im limbs), so the loads of a lane pair are contiguous.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "xbacksub.cuh"
+#include "xcolumn.cuh"
+#include "xqr_internal.h"
+
+namespace xb {
+
+constexpr int kG2Threads = 128;
+constexpr int kG2Warps = 4;
+constexpr int kG2Pairs = 64;  // lane pairs (rows per step) per CTA
+
+XB_DEVICE unsigned long long g2_timer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+XB_DEVICE int g2_ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+XB_DEVICE void g2_red_release(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int L, int RPP>
+struct g2 {
+    using R = real_t<L>;
+    using C = cx<R>;
+    static constexpr int L2 = 2 * L;
+
+    int m, n, ncol, cs, crank, tid, lane, warp, part, pair, gpair, row0, cnt;
+    double* ws;
+
+    XB_DEVICE double* col(int j) const { return ws + (int64_t)j * m * L2; }
+    // own half of row i of a column
+    XB_DEVICE R ld_part(const double* c, int i) const {
+        R v;
+        load_real<L>(c + ((int64_t)i * 2 + part) * L, 1, v);
+        return v;
+    }
+    XB_DEVICE R ld_part_cg(const double* c, int i, int p) const {
+        double t[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) t[l] = __ldcg(c + ((int64_t)i * 2 + p) * L + l);
+        R v;
+        load_real<L>(t, 1, v);
+        return v;
+    }
+    XB_DEVICE C ld_row(const double* c, int i) const {
+        C z;
+        load_real<L>(c + (int64_t)i * L2, 1, z.re);
+        load_real<L>(c + (int64_t)i * L2 + L, 1, z.im);
+        return z;
+    }
+    XB_DEVICE void st_part(double* c, int i, const R& v) const {
+        store_real<L>(c + ((int64_t)i * 2 + part) * L, 1, v);
+    }
+};
+
+// Cluster-wide fixed-order tree.  `acc` = this lane's in-lane partial (rows of
+// its pair; `have` = the pair owns at least one row).  Levels: lane pairs of a
+// warp (shuffle offsets 2, 4, 8, 16), then the cluster's 4*CS warp partials
+// through DSMEM (each warp redoes the top levels, so every lane ends with the
+// total of its own half; the other half is one shuffle away).
+template <int L, int RPP>
+XB_DEVICE real_t<L> g2_tree(const g2<L, RPP>& g, real_t<L> acc, double* slot_local, int buf) {
+    namespace cg = cooperative_groups;
+    using R = real_t<L>;
+    const int pi = g.lane >> 1;
+    // rolled loops: one copy of the add code, reused level after level (a
+    // single warp running straight-line code is instruction-fetch bound)
+#pragma unroll 1
+    for (int s = 1; s < 16; s <<= 1) {
+        R other = shfl_down_r(acc, 2 * s);
+        if ((pi & (2 * s - 1)) == 0 && (g.gpair + s) * RPP < g.m) acc = add(acc, other);
+    }
+    // slot[buf][warp][part] : L doubles
+    double* my = slot_local + ((buf * kG2Warps + g.warp) * 2) * L;
+    if (pi == 0) store_real<L>(my + g.part * L, 1, acc);
+    cg::this_cluster().sync();
+    const int np = kG2Warps * g.cs;          // warp partials in the cluster
+    const int npp = np > 16 ? np / 16 : 1;   // partials per pair (1 or 2)
+    const int rows_pp = 16 * RPP;            // rows covered by one warp partial
+    R v = acc;
+    int have = 0;
+    R st0 = acc;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        if (u >= npp) break;
+        const int k = pi * npp + u;
+        if (k < np && k * rows_pp < g.m) {
+            const double* rem = cg::this_cluster().map_shared_rank(slot_local, k / kG2Warps);
+            R w;
+            load_real<L>(rem + ((buf * kG2Warps + (k % kG2Warps)) * 2 + g.part) * L, 1, w);
+            if (u == 0) {
+                st0 = w;
+                have = 1;
+            } else {
+                st0 = add(st0, w);  // in-lane level (stride 1 partial)
+            }
+        }
+    }
+    v = st0;
+#pragma unroll 1
+    for (int s = 1; s < 16; s <<= 1) {
+        R other = shfl_down_r(v, 2 * s);
+        if ((pi & (2 * s - 1)) == 0 && (pi + s) * npp * rows_pp < g.m) v = add(v, other);
+    }
+    (void)have;
+    return shfl_idx_r(v, g.lane & 1);  // lane 0 holds re (or the real total), lane 1 im
+}
+
+template <int L, int RPP, bool LSQ>
+__global__ void __launch_bounds__(kG2Threads, 1) mgs_grid2_kernel(GridParams p) {
+    namespace cg = cooperative_groups;
+    using R = real_t<L>;
+    using C = cx<R>;
+    constexpr int L2 = 2 * L;
+
+    __shared__ double slot[2 * kG2Warps * 2 * L];
+    __shared__ int s_flag;
+
+    g2<L, RPP> g;
+    g.m = p.m;
+    g.n = p.n;
+    g.ncol = p.n + (LSQ ? 1 : 0);
+    g.cs = p.cs;
+    g.crank = (int)cg::this_cluster().block_rank();
+    g.tid = threadIdx.x;
+    g.lane = g.tid & 31;
+    g.warp = g.tid >> 5;
+    g.part = g.lane & 1;
+    g.pair = g.warp * 16 + (g.lane >> 1);
+    g.gpair = g.crank * kG2Pairs + g.pair;
+    g.row0 = g.gpair * RPP;
+    {
+        int c = g.m - g.row0;
+        g.cnt = c < 0 ? 0 : (c > RPP ? RPP : c);
+    }
+    g.ws = p.ws;
+    const int m = g.m, n = g.n, ncol = g.ncol;
+    const int cid = blockIdx.x / g.cs, G = gridDim.x / g.cs;
+    int buf = 0;
+
+    double* rdst = LSQ ? p.rws : p.r;
+    double* ydst = LSQ ? p.rws + (int64_t)n * n * L2 : nullptr;
+    auto record = [&](long long pos, int column, int code) {
+        atomicMin(p.key, status_key(pos, column, code));
+    };
+
+    // ---- copy owned columns into the workspace (AoS image); QR: zero strict lower R
+    for (int j = cid; j < ncol; j += G) {
+        const double* src = (j < n) ? p.a + (int64_t)j * m * L2 : p.b;
+        double* dst = g.col(j);
+        for (int e = g.crank * kG2Threads + g.tid; e < m * L2; e += g.cs * kG2Threads) dst[e] = src[e];
+        if (!LSQ && j < n && g.crank == 0)
+            for (int e = j + 1 + g.tid; e < n; e += kG2Threads)
+                for (int l = 0; l < L2; ++l) rdst[((int64_t)j * n + e) * L2 + l] = 0.0;
+    }
+    cg::this_cluster().sync();
+
+    // ---- norm pre-pass (mgs.hpp:91-96 / :143): column_norm of every column --
+    auto col_norm2 = [&](const double* c) -> R {
+        R acc = lane_tree<2, R>(g.cnt, [&](int t) {
+            C a = g.ld_row(c, g.row0 + t);
+            return cdot_re(a, a);
+        });
+        R s = g2_tree<L, RPP>(g, acc, slot, buf);
+        buf ^= 1;
+        return s;
+    };
+    for (int j = cid; j < ncol; j += G) {
+        R s = col_norm2(g.col(j));
+        R nrm = rsqrt_ref(s);
+        if (g.crank == 0 && g.tid == 0) {
+            if (!finite(head(s)) || !finite(head(nrm))) record(0, 0, XQR_OVERFLOW);
+            store_real<L>(p.norms + (int64_t)j * L, 1, nrm);
+        }
+    }
+    // grid-wide arrival (all CTAs are co-resident: cooperative launch)
+    __syncthreads();
+    if (g.tid == 0) {
+        __threadfence();
+        g2_red_release(p.counters, 1);
+        while (g2_ld_acquire(p.counters) < (int)gridDim.x) __nanosleep(64);
+    }
+    __syncthreads();
+    R thr;
+    {
+        R best = rmake<R>(0.0);
+        for (int j = 0; j < ncol; ++j) {
+            double t[L];
+#pragma unroll
+            for (int l = 0; l < L; ++l) t[l] = __ldcg(p.norms + (int64_t)j * L + l);
+            R v;
+            load_real<L>(t, 1, v);
+            if (lt(best, v)) best = v;
+        }
+        // breakdown_threshold (mgs.hpp:66-70)
+        thr = mul(rmake<R>((double)m * real_of<L>::eps), best);
+    }
+    const bool pre_err = __ldcg(p.key) != kNoError;
+    int* abortw = p.counters + 2;
+
+    // normalise column j (owner cluster) and publish it.  Returns false on error.
+    auto normalize_publish = [&](int j) -> bool {
+        double* c = g.col(j);
+        R s = col_norm2(c);
+        const bool tr = p.trace && g.tid == 0 && g.crank == 0;
+        if (tr) p.trace[j * 8 + 4] = g2_timer();
+        R rkk = rsqrt_ref(s);
+        if (tr) p.trace[j * 8 + 5] = g2_timer();
+        int code = 0;
+        if (!finite(head(s)) || !finite(head(rkk)))
+            code = XQR_OVERFLOW;
+        else if (le(rkk, thr))
+            code = XQR_BREAKDOWN;
+        recip_t<R> rc;
+        if (!code) {
+            int stc = 0;
+            rc = recip(rkk, stc);
+            code = stc;
+        }
+        if (tr) p.trace[j * 8 + 6] = g2_timer();
+        // code is cluster-uniform (same tree, same r_kk in every CTA); an
+        // overflow while dividing rows is local: it is recorded and stops the
+        // factorisation at the next round start, never in mid-round
+        bool ok = true;
+        if (!code) {
+            for (int t = 0; t < g.cnt; ++t) {
+                R v = divide(g.ld_part(c, g.row0 + t), rkk, rc);
+                if (!finite(head(v))) ok = false;
+                g.st_part(c, g.row0 + t, v);
+            }
+        }
+        ok = __syncthreads_and(ok);
+        if (tr) p.trace[j * 8 + 7] = g2_timer();
+        if (g.tid == 0) {
+            if (code || !ok) {
+                record(1 + (long long)j * (ncol + 1), code == XQR_BREAKDOWN ? j + 1 : 0,
+                       code ? code : XQR_OVERFLOW);
+                atomicExch(abortw, 1);
+            } else if (g.crank == 0) {
+                C d{rkk, rmake<R>(0.0)};
+                store_aos<L>(rdst + ((int64_t)j * n + j) * L2, d);
+            }
+            __threadfence();
+            g2_red_release(p.flags + j, 1);
+            if (p.trace && g.crank == 0) p.trace[j * 8 + 2] = g2_timer();
+        }
+        return code == 0;
+    };
+
+    bool abort = pre_err;
+    if (!abort && cid == 0) abort = !normalize_publish(0);
+    if (pre_err && blockIdx.x == 0 && g.tid == 0) atomicExch(abortw, 1);
+
+    // ---- MGS rounds ----------------------------------------------------------------
+    for (int k = 0; k < n && !abort; ++k) {
+        const int j0 = k + 1 + ((cid - (k + 1)) % G + G) % G;
+        if (j0 >= ncol) continue;
+        // cluster-uniform decision: rank 0 acquires q_k (or sees the abort
+        // word), the cluster barrier hands the verdict to every CTA
+        if (g.crank == 0 && g.tid == 0) {
+            int v;
+            while ((v = g2_ld_acquire(p.flags + k)) < g.cs && g2_ld_acquire(abortw) == 0) {
+            }
+            s_flag = (v >= g.cs && g2_ld_acquire(abortw) == 0) ? 1 : 0;
+        }
+        cg::this_cluster().sync();
+        if (*cg::this_cluster().map_shared_rank(&s_flag, 0) == 0) {
+            abort = true;
+            break;
+        }
+        // q_k rows of this lane pair, both halves, in registers
+        C q[RPP];
+        const double* qk = g.col(k);
+#pragma unroll
+        for (int t = 0; t < RPP; ++t)
+            if (t < g.cnt) {
+                q[t].re = g.ld_part_cg(qk, g.row0 + t, 0);
+                q[t].im = g.ld_part_cg(qk, g.row0 + t, 1);
+            }
+        if (p.trace && g.tid == 0 && g.crank == 0 && j0 == k + 1) p.trace[(k + 1) * 8 + 0] = g2_timer();
+        const long long pos_k = 1 + (long long)k * (ncol + 1);
+        for (int j = j0; j < ncol; j += G) {
+            double* c = g.col(j);
+            // r_kj = q_k^H a_j (reduction.hpp:45-51): this lane's half of the
+            // complex leaf cmul(conj(q), a) (complex.hpp:41-44), operands
+            // selected so both halves run the same code
+            R acc = lane_tree<2, R>(g.cnt, [&](int t) {
+                C a = g.ld_row(c, g.row0 + t);
+                const R y1 = g.part ? a.im : a.re, y2 = g.part ? a.re : a.im;
+                rpair<R> pr = mul2(q[t].re, y1, neg(q[t].im), y2);
+                return add(pr.x, g.part ? pr.y : neg(pr.y));
+            });
+            R rh = g2_tree<L, RPP>(g, acc, slot, buf);
+            buf ^= 1;
+            C r;
+            R ro = shfl_xor_r(rh, 1);
+            r.re = g.part ? ro : rh;
+            r.im = g.part ? rh : ro;
+            bool ok = finite(head(r.re)) && finite(head(r.im));
+            // a_i -= r * q_i (mgs.hpp:59): t = cmul(r, q_i), a - t
+            for (int t = 0; t < g.cnt; ++t) {
+                const R y1 = g.part ? q[t].im : q[t].re, y2 = g.part ? q[t].re : q[t].im;
+                rpair<R> pr = mul2(r.re, y1, r.im, y2);
+                R tt = add(pr.x, g.part ? pr.y : neg(pr.y));
+                R v = sub(g.ld_part(c, g.row0 + t), tt);
+                if (!finite(head(v))) ok = false;
+                g.st_part(c, g.row0 + t, v);
+            }
+            ok = __syncthreads_and(ok);
+            if (g.tid < 2 && g.crank == 0) {
+                // lanes 0 / 1 hold re / im of r; write r_kj (or y_k)
+                double* dst = (j < n) ? rdst + ((int64_t)j * n + k) * L2 : ydst + (int64_t)k * L2;
+                store_real<L>(dst + g.part * L, 1, rh);
+                if (!ok && g.tid == 0) record(pos_k + (j - k), 0, XQR_OVERFLOW);
+            }
+            if (!ok && g.tid == 0) atomicExch(abortw, 1);
+            if (p.trace && g.tid == 0 && g.crank == 0 && j == k + 1) p.trace[(k + 1) * 8 + 1] = g2_timer();
+            if (j == k + 1 && j < n) {
+                if (!normalize_publish(j)) {
+                    abort = true;
+                    break;
+                }
+            }
+        }
+        if (p.trace && g.tid == 0) atomicMax(p.trace + (k + 1) * 8 + 3, g2_timer());
+    }
+
+    // z = column_norm(b) by its owner (mgs.hpp:155)
+    if (LSQ && !abort && (n % G) == cid) {
+        R s = col_norm2(g.col(n));
+        R z = rsqrt_ref(s);
+        if (g.tid == 0 && g.crank == 0) {
+            if (!finite(head(s)) || !finite(head(z))) record(1 + (long long)n * (ncol + 1), 0, XQR_OVERFLOW);
+            store_real<L>(p.z, 1, z);
+        }
+    }
+    if (!LSQ) {
+        // Q = the normalised owned columns (the workspace is the AoS image)
+        // (each lane copies the halves it wrote itself: no cluster barrier needed)
+        for (int j = cid; j < n; j += G) {
+            const double* src = g.col(j);
+            double* dst = p.q + (int64_t)j * m * L2;
+            for (int t = 0; t < g.cnt; ++t) g.st_part(dst, g.row0 + t, g.ld_part(src, g.row0 + t));
+        }
+    }
+    // no CTA may exit while a cluster peer can still read its shared memory
+    cg::this_cluster().sync();
+    // everyone done -> CTA 0 runs the fused back substitution
+    __syncthreads();
+    if (g.tid == 0) {
+        __threadfence();
+        g2_red_release(p.counters + 1, 1);
+    }
+    if (blockIdx.x == 0) {
+        __shared__ unsigned long long s_key;
+        if (g.tid == 0) {
+            while (g2_ld_acquire(p.counters + 1) < (int)gridDim.x) __nanosleep(64);
+            s_key = __ldcg(p.key);
+        }
+        __syncthreads();
+        if (LSQ && s_key == kNoError) {
+            // mgs.hpp:157 -> :110-126; x in (dynamic) shared memory
+            extern __shared__ double xs[];
+            double* prep = p.rws + (int64_t)n * n * L2 + (int64_t)n * L2;
+            bool bad = cta_back_substitute<L>(n, p.rws, ydst, xs, prep, &s_key,
+                                              2 + (long long)n * (ncol + 1));
+            if (!bad)
+                for (int e = g.tid; e < n * L2; e += kG2Threads) p.x[e] = xs[e];
+            __syncthreads();
+        }
+        if (g.tid == 0) {
+            unsigned long long key = s_key;
+            xqr_status st;
+            st.system = 0;
+            st.code = key == kNoError ? 0 : (int)(key & 15);
+            st.column = key == kNoError ? 0 : (int)((key >> 4) & 0xFFFFF);
+            *p.st = st;
+        }
+    }
+}
+
+template <int L, int RPP, bool LSQ>
+cudaError_t launch_grid2_t(const GridParams& p, int max_clusters, cudaStream_t s) {
+    auto kern = mgs_grid2_kernel<L, RPP, LSQ>;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.blockDim = dim3(kG2Threads, 1, 1);
+    // x of the back substitution lives here (CTA 0); the size also keeps the
+    // kernel at ONE CTA per SM, so each warp has an SM sub-partition to itself
+    cfg.dynamicSmemBytes = sizeof(double) * (size_t)p.n * 2 * L;
+    if (cfg.dynamicSmemBytes < 120 * 1024) cfg.dynamicSmemBytes = 120 * 1024;
+    if (cfg.dynamicSmemBytes > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)cfg.dynamicSmemBytes);
+        if (e != cudaSuccess) return e;
+    }
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    // as many clusters as fit co-resident (and no more than there are columns)
+    int nclusters = 0;
+    cfg.gridDim = dim3(p.cs, 1, 1);
+    if (p.cs > 8) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, (void*)kern, &cfg);
+    if (e != cudaSuccess) return e;
+    const int ncol = p.n + (LSQ ? 1 : 0);
+    if (nclusters > max_clusters) nclusters = max_clusters;
+    if (nclusters > ncol) nclusters = ncol;
+    if (nclusters < 1) return cudaErrorInvalidConfiguration;
+    cfg.gridDim = dim3(nclusters * p.cs, 1, 1);
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <int L>
+cudaError_t launch_grid2(const GridParams& p, bool lsq, int max_clusters, cudaStream_t s) {
+    switch (p.rpt) {
+        case 1: return lsq ? launch_grid2_t<L, 1, true>(p, max_clusters, s)
+                           : launch_grid2_t<L, 1, false>(p, max_clusters, s);
+        case 2: return lsq ? launch_grid2_t<L, 2, true>(p, max_clusters, s)
+                           : launch_grid2_t<L, 2, false>(p, max_clusters, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace xb

@@ -67,10 +67,11 @@ struct BackSubParams {
 };
 cudaError_t launch_back_substitute(int limbs, const BackSubParams& p, cudaStream_t s);
 
-// Single-system grid kernel (xgrid.cuh): one persistent cooperative CTA per SM.
+// Single-system cluster grid kernel (xgrid2.cuh): a column per cluster of
+// `cs` CTAs of 128 threads, a lane pair per row (rpt = rows per lane pair).
 struct GridParams {
     int m, n;
-    int rpt;            // rows per thread (power of two)
+    int rpt;            // rows per lane pair (1 or 2)
     const double* a;    // AoS m x n
     const double* b;    // AoS m (LS)
     double* q;          // AoS out (QR)
@@ -78,23 +79,27 @@ struct GridParams {
     double* x;          // AoS out n (LS)
     double* z;          // L doubles (LS)
     xqr_status* st;
-    double* ws;         // planar columns, ncol * COL doubles
+    double* ws;         // AoS working copy, ncol * m * 2L doubles
     double* rws;        // LS: R (n*n*2L) + y (n*2L) + Smith prep (n*(3L+1))
     double* norms;      // ncol * L
-    int* flags;         // n: 0 pending, 1 published, 2 abort
-    unsigned long long* key;  // global status key (init kNoError)
+    int* flags;         // n: arrivals of the owner cluster's CTAs
+    unsigned long long* key;    // global status key (init kNoError)
     unsigned long long* trace;  // optional (dev): 4 globaltimer stamps per pivot
+    int cs;                     // CTAs per cluster
+    int* counters;              // [0] pre-pass arrivals, [1] final arrivals, [2] abort word
 };
 
-constexpr int kGridRowsPerThreadMax = 4;  // m <= 1024
-inline int rows_per_thread(int m) {
-    int r = 1;
-    while (256 * r < m) r <<= 1;
-    return r;
+constexpr int kGridMaxRows = 1024;  // 8 CTAs x 64 lane pairs x 2 rows
+inline void grid_shape(int m, int& cs, int& rpp) {
+    const int need = (m + 63) / 64;
+    cs = 1;
+    while (cs < need && cs < 8) cs <<= 1;
+    rpp = 1;
+    while (cs * 64 * rpp < m) rpp <<= 1;
 }
-cudaError_t launch_grid_L1(const GridParams& p, int grid, bool lsq, cudaStream_t s);
-cudaError_t launch_grid_L2(const GridParams& p, int grid, bool lsq, cudaStream_t s);
-cudaError_t launch_grid_L4(const GridParams& p, int grid, bool lsq, cudaStream_t s);
+cudaError_t launch_grid_L1(const GridParams& p, int max_clusters, bool lsq, cudaStream_t s);
+cudaError_t launch_grid_L2(const GridParams& p, int max_clusters, bool lsq, cudaStream_t s);
+cudaError_t launch_grid_L4(const GridParams& p, int max_clusters, bool lsq, cudaStream_t s);
 
 cudaError_t launch_arith(int limbs, int op, int64_t count, const double* a, const double* b,
                          double* out, int32_t* codes, cudaStream_t s);

@@ -47,7 +47,7 @@ def host():
 @pytest.mark.parametrize("op", [0, 1, 2, 3, 4, 5, 6, 7, 8])
 def test_host_arith_bitwise(port, host, L, op):
     rng = np.random.default_rng(7000 + 10 * L + op)
-    count = {0: 60000, 1: 60000, 2: 60000, 7: 30000, 5: 12000}.get(op, 6000)
+    count = {0: 400000, 1: 200000, 2: 60000, 7: 60000, 5: 12000}.get(op, 6000)
     cplx = 5 <= op <= 7
     renorm = lambda x: port.arith(L, 8, x)[0]
     a, b = operand_pairs(rng, count, L, renorm, parts=2 if cplx else 1)

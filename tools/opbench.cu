@@ -111,19 +111,19 @@ void run(const char* name, double fp64_per_op, int blocks_per_sm, int sms, doubl
 
 // latency: one warp, one dependent chain; ns per op
 template <class R, int OP>
-void lat(const char* name, double* sink) {
+void lat(const char* name, double* sink, int blocks = 1, int threads = 32) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    bench<R, OP, 1><<<1, 32>>>(sink, 1);
+    bench<R, OP, 1><<<blocks, threads>>>(sink, 1);
     cudaEventRecord(e0);
-    bench<R, OP, 1><<<1, 32>>>(sink, 16);
+    bench<R, OP, 1><<<blocks, threads>>>(sink, 16);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     const double ns = ms * 1e6 / (16.0 * K);
-    printf("latency %-10s %8.1f ns/op  (%6.0f cycles at 1.965 GHz)\n", name, ns, ns * 1.965);
+    printf("latency %-10s %4dx%-4d %8.1f ns/op  (%6.0f cycles at 1.965 GHz)\n", name, blocks, threads, ns, ns * 1.965);
 }
 
 int main() {
@@ -134,6 +134,10 @@ int main() {
     // reference per-op FP64 instruction weights (Appendix B): qd add 90, mul 179,
     // cmul 896, cadd 180; dd add 20, mul 9, cmul 76, cadd 40
     lat<r4, 0>("qd add", sink);
+    lat<r4, 0>("qd add", sink, 1, 128);
+    lat<r4, 0>("qd add", sink, 148, 128);
+    lat<r4, 0>("qd add", sink, 148, 64);
+    lat<r4, 1>("qd mul", sink, 148, 128);
     lat<r4, 1>("qd mul", sink);
     lat<r4, 2>("qd cmul", sink);
     lat<r4, 3>("qd cadd", sink);
