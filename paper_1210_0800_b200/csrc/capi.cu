@@ -25,6 +25,12 @@ struct xqr_ctx {
     size_t pinned_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool timed = false;
+    // host-buffer batched calls: a second stream and slot events for the
+    // copy / compute pipeline (created on first use)
+    cudaStream_t stream2 = nullptr;
+    cudaEvent_t slot_done[2] = {nullptr, nullptr};
+    void* pinned_out = nullptr;
+    size_t pinned_out_bytes = 0;
     int64_t launches = 0;
     int num_sms = 148;
     bool coop = false;
@@ -272,6 +278,10 @@ void xqr_ctx_destroy(xqr_ctx* ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+    for (auto& ev : ctx->slot_done)
+        if (ev) cudaEventDestroy(ev);
+    if (ctx->pinned_out) cudaFreeHost(ctx->pinned_out);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -346,6 +356,172 @@ int xqr_back_substitute_batched_device(xqr_ctx* ctx, int limbs, int64_t batch, i
 }
 
 // ---- host entry points -----------------------------------------------------------
+namespace {
+
+bool is_pinned(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// CTA kernel on `batch` systems, on an explicit stream and scratch region.
+int launch_cta_batch(xqr_ctx* ctx, cudaStream_t s, bool lsq, int limbs, int64_t batch, int m, int n,
+                     const double* d_a, const double* d_b, double* d_q, double* d_r, double* d_x,
+                     double* d_z, xqr_status* d_st, double* scratch) {
+    const int ncol = n + (lsq ? 1 : 0);
+    xb::SolveParams p{};
+    p.batch = batch;
+    p.m = m;
+    p.n = n;
+    p.a = d_a;
+    p.b = d_b;
+    p.q = d_q;
+    p.r = d_r;
+    p.x = d_x;
+    p.z = d_z;
+    p.st = d_st;
+    p.ws_stride = xb::ws_doubles(limbs, m, ncol);
+    p.rws_stride = lsq ? xb::rws_doubles(limbs, n) : 0;
+    p.ws = scratch;
+    p.rws = lsq ? scratch + (size_t)batch * p.ws_stride : nullptr;
+    cudaError_t e = xb::launch_mgs_cta(limbs, lsq, p, s);
+    ctx->launches += 1;
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "mgs kernel launch");
+    return 0;
+}
+
+// Host-buffer batch: split into chunks of about one wave of the CTA kernel
+// and pipeline them over two streams, so the host->device copy of chunk c+1
+// (straight from the caller's buffer when it is pinned, else through a
+// pinned staging slot) overlaps the solve of chunk c.
+int solve_host_batched(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t m, int64_t n,
+                       const double* a, const double* b, double* q, double* r, double* x, double* z,
+                       xqr_status* st) {
+    const size_t L2 = 2 * (size_t)limbs;
+    const int ncol = (int)n + (lsq ? 1 : 0);
+    int64_t chunk = 4 * (int64_t)ctx->num_sms;
+    if (const char* e = std::getenv("XQR_CHUNK")) chunk = std::max<int64_t>(1, std::atoll(e));
+    if (chunk > batch) chunk = batch;
+    const int64_t nchunks = (batch + chunk - 1) / chunk;
+    // per-system sizes (doubles)
+    const size_t sa = (size_t)m * n * L2, sb = lsq ? (size_t)m * L2 : 0, sq = lsq ? 0 : sa,
+                 sr = lsq ? 0 : (size_t)n * n * L2, sx = lsq ? (size_t)n * L2 : 0, sz = lsq ? limbs : 0;
+    const size_t sws = xb::ws_doubles(limbs, (int)m, ncol) + (lsq ? xb::rws_doubles(limbs, (int)n) : 0);
+    const size_t sout = sq + sr + sx + sz;  // doubles out per system
+    arena_plan plan;
+    size_t o_in[2], o_out[2], o_st[2], o_ws[2];
+    for (int k = 0; k < 2; ++k) {
+        o_in[k] = plan.add(sizeof(double) * chunk * (sa + sb));
+        o_out[k] = plan.add(sizeof(double) * chunk * sout);
+        o_st[k] = plan.add(sizeof(xqr_status) * chunk);
+        o_ws[k] = plan.add(sizeof(double) * chunk * sws);
+    }
+    cudaError_t e = ensure_arena(ctx, plan.total + 256);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
+    if (!ctx->stream2) {
+        e = cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return set_cuda_error(ctx, e, "stream");
+        for (auto& ev : ctx->slot_done) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    }
+    const bool pin_a = is_pinned(a) && (!lsq || is_pinned(b));
+    if (!pin_a) {
+        e = ensure_pinned(ctx, 2 * sizeof(double) * chunk * (sa + sb));
+        if (e != cudaSuccess) return set_cuda_error(ctx, e, "pinned staging allocation");
+    }
+    // outputs land in pinned staging (2 slots), copied out once a slot is reused / at the end
+    {
+        const size_t need = 2 * (sizeof(double) * chunk * sout + sizeof(xqr_status) * chunk);
+        if (need > ctx->pinned_out_bytes) {
+            if (ctx->pinned_out) cudaFreeHost(ctx->pinned_out);
+            ctx->pinned_out = nullptr;
+            ctx->pinned_out_bytes = 0;
+            e = cudaMallocHost(&ctx->pinned_out, need);
+            if (e != cudaSuccess) return set_cuda_error(ctx, e, "pinned output allocation");
+            ctx->pinned_out_bytes = need;
+        }
+    }
+    cudaStream_t streams[2] = {ctx->stream, ctx->stream2};
+    // the caller's stream may have pending work (e.g. torch): order stream2 after it
+    cudaEventRecord(ctx->slot_done[1], ctx->stream);
+    cudaStreamWaitEvent(ctx->stream2, ctx->slot_done[1], 0);
+    int64_t pending[2] = {-1, -1};  // chunk index whose outputs sit in slot k
+    std::vector<xqr_status> hst(batch);
+    auto out_slot = [&](int k) {
+        return static_cast<char*>(ctx->pinned_out) + k * (sizeof(double) * chunk * sout + sizeof(xqr_status) * chunk);
+    };
+    auto drain = [&](int k) -> int {
+        if (pending[k] < 0) return 0;
+        cudaError_t ee = cudaEventSynchronize(ctx->slot_done[k]);
+        if (ee != cudaSuccess) return set_cuda_error(ctx, ee, "solve");
+        const int64_t c = pending[k], s0 = c * chunk, cs = std::min(chunk, batch - s0);
+        const double* src = reinterpret_cast<const double*>(out_slot(k));
+        if (lsq) {
+            std::memcpy(x + s0 * sx, src, sizeof(double) * cs * sx);
+            std::memcpy(z + s0 * sz, src + cs * sx, sizeof(double) * cs * sz);
+        } else {
+            std::memcpy(q + s0 * sq, src, sizeof(double) * cs * sq);
+            std::memcpy(r + s0 * sr, src + cs * sq, sizeof(double) * cs * sr);
+        }
+        const xqr_status* sst = reinterpret_cast<const xqr_status*>(out_slot(k) + sizeof(double) * chunk * sout);
+        for (int64_t i = 0; i < cs; ++i) {
+            hst[s0 + i] = sst[i];
+            hst[s0 + i].system = s0 + i;
+        }
+        pending[k] = -1;
+        return 0;
+    };
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int k = (int)(c & 1);
+        cudaStream_t s = streams[k];
+        const int64_t s0 = c * chunk, cs = std::min(chunk, batch - s0);
+        if (int rc = drain(k)) return rc;  // slot k free again
+        double* d_in = reinterpret_cast<double*>(at(ctx, o_in[k]));
+        double* d_out = reinterpret_cast<double*>(at(ctx, o_out[k]));
+        xqr_status* d_st = reinterpret_cast<xqr_status*>(at(ctx, o_st[k]));
+        const double* src_a = a + s0 * sa;
+        const double* src_b = lsq ? b + s0 * sb : nullptr;
+        if (!pin_a) {
+            double* stage = static_cast<double*>(ctx->pinned) + (size_t)k * chunk * (sa + sb);
+            std::memcpy(stage, src_a, sizeof(double) * cs * sa);
+            if (lsq) std::memcpy(stage + cs * sa, src_b, sizeof(double) * cs * sb);
+            src_a = stage;
+            src_b = stage + cs * sa;
+        }
+        cudaMemcpyAsync(d_in, src_a, sizeof(double) * cs * sa, cudaMemcpyHostToDevice, s);
+        if (lsq) cudaMemcpyAsync(d_in + cs * sa, src_b, sizeof(double) * cs * sb, cudaMemcpyHostToDevice, s);
+        double *dq = nullptr, *dr = nullptr, *dx = nullptr, *dz = nullptr;
+        if (lsq) {
+            dx = d_out;
+            dz = d_out + cs * sx;
+        } else {
+            dq = d_out;
+            dr = d_out + cs * sq;
+        }
+        int rc = launch_cta_batch(ctx, s, lsq, limbs, cs, (int)m, (int)n, d_in, lsq ? d_in + cs * sa : nullptr,
+                                  dq, dr, dx, dz, d_st, reinterpret_cast<double*>(at(ctx, o_ws[k])));
+        if (rc) return rc;
+        cudaMemcpyAsync(out_slot(k), d_out, sizeof(double) * cs * sout, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(out_slot(k) + sizeof(double) * chunk * sout, d_st, sizeof(xqr_status) * cs,
+                        cudaMemcpyDeviceToHost, s);
+        cudaEventRecord(ctx->slot_done[k], s);
+        pending[k] = c;
+    }
+    for (int k = 0; k < 2; ++k)
+        if (int rc = drain(k)) return rc;
+    // later work on the ctx stream is ordered after both streams
+    cudaEventRecord(ctx->slot_done[1], ctx->stream2);
+    cudaStreamWaitEvent(ctx->stream, ctx->slot_done[1], 0);
+    ctx->timed = false;
+    if (st) std::memcpy(st, hst.data(), sizeof(xqr_status) * batch);
+    return first_code(hst);
+}
+
+}  // namespace
+
 static int solve_host(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t m, int64_t n,
                       const double* a, const double* b, double* q, double* r, double* x, double* z,
                       xqr_status* st) {
@@ -356,6 +532,7 @@ static int solve_host(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t 
     }
     if (batch == 0) return 0;
     cudaSetDevice(ctx->device);
+    if (batch > 1) return solve_host_batched(ctx, lsq, limbs, batch, m, n, a, b, q, r, x, z, st);
     const size_t L2 = 2 * (size_t)limbs;
     const size_t a_b = sizeof(double) * batch * m * n * L2;
     const size_t b_b = lsq ? sizeof(double) * batch * m * L2 : 0;

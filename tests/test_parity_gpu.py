@@ -224,6 +224,39 @@ def test_batched_matches_single(port, L):
             assert_same(r[s], wr)
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+def test_batched_pipeline_chunks(port, monkeypatch, pinned):
+    """The host-buffer batch is split into chunks pipelined over two streams
+    (capi.cu solve_host_batched); force small, uneven chunks and check every
+    system, its status index, and the pinned (direct DMA) input path."""
+    import torch
+
+    L, batch, m, n = 4, 23, 12, 9
+    a = np.zeros((batch, n, m, 2, L))
+    b = np.zeros((batch, m, 2, L))
+    for s in range(batch):
+        a[s], b[s] = port.gen_system(L, m, n, 1.0, 9, s)
+    a[17, 4] = a[17, 1]  # breakdown at column 5
+    if pinned:
+        a = torch.from_numpy(a).pin_memory().numpy()
+        b = torch.from_numpy(b).pin_memory().numpy()
+    monkeypatch.setenv("XQR_CHUNK", "5")
+    x, z, codes, cols = xqr.lsq_solve_batched(a, b)
+    q, r, qcodes, qcols = xqr.mgs_qr_batched(a)
+    for s in range(batch):
+        wx, wz, st = port.lsq_solve(a[s], b[s])
+        assert (codes[s], cols[s]) == st, s
+        if st[0] == 0:
+            assert_same(x[s], wx, f"x[{s}]")
+            assert_same(z[s], wz, f"z[{s}]")
+        wq, wr, st = port.mgs_qr(a[s])
+        assert (qcodes[s], qcols[s]) == st, s
+        if st[0] == 0:
+            assert_same(q[s], wq, f"q[{s}]")
+            assert_same(r[s], wr, f"r[{s}]")
+    assert codes[17] == 1 and cols[17] == 5
+
+
 def test_par_api_routes_to_device(port):
     a, b = port.gen_system(2, 33, 33, 1.0, 7)
     x, z, _ = port.lsq_solve(a, b)
