@@ -128,9 +128,14 @@ bool use_grid_path(xqr_ctx* ctx, int m, int n) {
     return ctx->coop && n >= 8 && m >= 64 && m <= xb::kGridMaxRows;
 }
 
+size_t grid_ws_doubles(int limbs, int m, int ncol) {
+    if (limbs <= 2) return (size_t)ncol * 2 * limbs * 256 * xb::grid1_rows_per_thread(m);
+    return (size_t)ncol * m * 2 * limbs;
+}
+
 size_t grid_scratch_bytes(bool lsq, int limbs, int m, int n) {
     const int ncol = n + (lsq ? 1 : 0);
-    return sizeof(double) * ((size_t)ncol * m * 2 * limbs + (lsq ? xb::rws_doubles(limbs, n) : 0) +
+    return sizeof(double) * (grid_ws_doubles(limbs, m, ncol) + (lsq ? xb::rws_doubles(limbs, n) : 0) +
                              (size_t)ncol * limbs) +
            sizeof(int) * ((size_t)n + 4) + sizeof(unsigned long long) * (8 * (size_t)(n + 1) + 1) +
            8 * 256;
@@ -143,7 +148,12 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     xb::GridParams p{};
     p.m = m;
     p.n = n;
-    xb::grid_shape(m, p.cs, p.rpt);
+    if (limbs <= 2) {
+        p.cs = 1;
+        p.rpt = xb::grid1_rows_per_thread(m);
+    } else {
+        xb::grid_shape(m, p.cs, p.rpt);
+    }
     p.a = d_a;
     p.b = d_b;
     p.q = d_q;
@@ -152,7 +162,7 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     p.z = d_z;
     p.st = d_st;
     arena_plan plan;
-    const size_t o_ws = plan.add(sizeof(double) * (size_t)ncol * m * 2 * limbs);
+    const size_t o_ws = plan.add(sizeof(double) * grid_ws_doubles(limbs, m, ncol));
     const size_t o_rws = plan.add(lsq ? sizeof(double) * xb::rws_doubles(limbs, n) : 0);
     const size_t o_nrm = plan.add(sizeof(double) * (size_t)ncol * limbs);
     const size_t o_flg = plan.add(sizeof(int) * ((size_t)n + 4));
@@ -174,8 +184,8 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     const int max_clusters = ctx->num_sms / p.cs;
     if (timed) cudaEventRecord(ctx->ev0, ctx->stream);
     switch (limbs) {
-        case 1: e = xb::launch_grid_L1(p, max_clusters, lsq, ctx->stream); break;
-        case 2: e = xb::launch_grid_L2(p, max_clusters, lsq, ctx->stream); break;
+        case 1: e = xb::launch_grid_L1(p, std::min(ncol, ctx->num_sms), lsq, ctx->stream); break;
+        case 2: e = xb::launch_grid_L2(p, std::min(ncol, ctx->num_sms), lsq, ctx->stream); break;
         default: e = xb::launch_grid_L4(p, max_clusters, lsq, ctx->stream); break;
     }
     if (timed) cudaEventRecord(ctx->ev1, ctx->stream);

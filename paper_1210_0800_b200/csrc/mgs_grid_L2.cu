@@ -1,8 +1,8 @@
-// mgs_grid_L2.cu -- instantiation unit for the single-system cluster grid kernel (xgrid2.cuh).
-#include "xgrid2.cuh"
+// mgs_grid_L2.cu -- instantiation unit for the single-system grid kernel (xgrid1.cuh).
+#include "xgrid1.cuh"
 
 namespace xb {
-cudaError_t launch_grid_L2(const GridParams& p, int max_clusters, bool lsq, cudaStream_t s) {
-    return launch_grid2<2>(p, lsq, max_clusters, s);
+cudaError_t launch_grid_L2(const GridParams& p, int grid, bool lsq, cudaStream_t s) {
+    return lsq ? launch_grid1<2, true>(p, grid, s) : launch_grid1<2, false>(p, grid, s);
 }
 }  // namespace xb

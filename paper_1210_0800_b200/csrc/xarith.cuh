@@ -734,14 +734,10 @@ XB_DEV r4 add_merge_pred(const r4& a, const r4& b) {
 // merges, else the reference merge (one call, so the inlined fast path stays
 // small).
 XB_GEN r4 add_slow(const r4 a, const r4 b) {
-#if defined(XB_ADD_SLOW_BRANCHY)
     bool ok;
     r4 r = add_alt_fast(a, b, ok);
-    if (!ok) r = add_general(a, b);
+    if (!ok) r = add_merge_pred(a, b);
     return r;
-#else
-    return add_merge_pred(a, b);
-#endif
 }
 
 XB_OP4 r4 add(const r4 a, const r4 b) {

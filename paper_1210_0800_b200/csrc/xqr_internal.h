@@ -71,7 +71,7 @@ cudaError_t launch_back_substitute(int limbs, const BackSubParams& p, cudaStream
 // `cs` CTAs of 128 threads, a lane pair per row (rpt = rows per lane pair).
 struct GridParams {
     int m, n;
-    int rpt;            // rows per lane pair (1 or 2)
+    int rpt;            // xgrid2: rows per lane pair (1 or 2); xgrid1: rows per thread
     const double* a;    // AoS m x n
     const double* b;    // AoS m (LS)
     double* q;          // AoS out (QR)
@@ -79,7 +79,7 @@ struct GridParams {
     double* x;          // AoS out n (LS)
     double* z;          // L doubles (LS)
     xqr_status* st;
-    double* ws;         // AoS working copy, ncol * m * 2L doubles
+    double* ws;         // xgrid2: AoS working copy (ncol * m * 2L); xgrid1: planar columns
     double* rws;        // LS: R (n*n*2L) + y (n*2L) + Smith prep (n*(3L+1))
     double* norms;      // ncol * L
     int* flags;         // n: arrivals of the owner cluster's CTAs
@@ -89,7 +89,8 @@ struct GridParams {
     int* counters;              // [0] pre-pass arrivals, [1] final arrivals, [2] abort word
 };
 
-constexpr int kGridMaxRows = 1024;  // 8 CTAs x 64 lane pairs x 2 rows
+constexpr int kGridMaxRows = 1024;
+// quad-double (xgrid2.cuh): CTAs per cluster and rows per lane pair
 inline void grid_shape(int m, int& cs, int& rpp) {
     const int need = (m + 63) / 64;
     cs = 1;
@@ -97,8 +98,14 @@ inline void grid_shape(int m, int& cs, int& rpp) {
     rpp = 1;
     while (cs * 64 * rpp < m) rpp <<= 1;
 }
-cudaError_t launch_grid_L1(const GridParams& p, int max_clusters, bool lsq, cudaStream_t s);
-cudaError_t launch_grid_L2(const GridParams& p, int max_clusters, bool lsq, cudaStream_t s);
+// double / double-double (xgrid1.cuh): rows per thread of a 256-thread CTA
+inline int grid1_rows_per_thread(int m) {
+    int r = 1;
+    while (256 * r < m) r <<= 1;
+    return r;
+}
+cudaError_t launch_grid_L1(const GridParams& p, int grid, bool lsq, cudaStream_t s);
+cudaError_t launch_grid_L2(const GridParams& p, int grid, bool lsq, cudaStream_t s);
 cudaError_t launch_grid_L4(const GridParams& p, int max_clusters, bool lsq, cudaStream_t s);
 
 cudaError_t launch_arith(int limbs, int op, int64_t count, const double* a, const double* b,
