@@ -153,6 +153,11 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
         p.rpt = xb::grid1_rows_per_thread(m);
     } else {
         xb::grid_shape(m, p.cs, p.rpt);
+        if (const char* e = std::getenv("XQR_GRID_CS")) {  // dev override of the cluster size
+            p.cs = std::max(1, std::min(8, std::atoi(e)));
+            p.rpt = 1;
+            while (p.cs * 64 * p.rpt < m) p.rpt <<= 1;
+        }
     }
     p.a = d_a;
     p.b = d_b;

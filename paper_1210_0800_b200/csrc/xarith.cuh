@@ -864,6 +864,15 @@ XB_OP4 r4 mul(const r4 a, const r4 b) {
     return r;
 }
 
+// Always-call forms of the qd add / multiply, for the latency-bound scalar
+// chains (Newton iterations, reduction trees, pivot divisions): one shared
+// copy of each operation stays hot in the instruction cache of a lone warp.
+XB_CALL_IF r4 addc(const r4 a, const r4 b) { return add(a, b); }
+XB_CALL_IF r4 mulc(const r4 a, const r4 b) { return mul(a, b); }
+XB_DEV r4 subc(const r4& a, const r4& b) { return addc(a, neg(b)); }
+XB_DEV r1 addc(const r1& a, const r1& b) { return add(a, b); }
+XB_DEV r2 addc(const r2& a, const r2& b) { return add(a, b); }
+
 XB_DEV r4 mul_pwr2(const r4& a, double p2) {  // :341-343
     return {dmul(a.c0, p2), dmul(a.c1, p2), dmul(a.c2, p2), dmul(a.c3, p2)};
 }
@@ -873,11 +882,11 @@ XB_OP2 r4 rsqrt_ref(const r4 a) {
     r4 x = make4(ddiv(1.0, dsqrt(a.c0)));
 #pragma unroll 1
     for (int it = 0; it < 2; ++it) {
-        r4 t = mul(a, x);
-        x = add(x, mul_pwr2(mul(x, sub(make4(1.0), mul(t, x))), 0.5));
+        r4 t = mulc(a, x);
+        x = addc(x, mul_pwr2(mulc(x, subc(make4(1.0), mulc(t, x))), 0.5));
     }
-    r4 y = mul(a, x);
-    y = add(y, mul_pwr2(mul(sub(a, mul(y, y)), x), 0.5));
+    r4 y = mulc(a, x);
+    y = addc(y, mul_pwr2(mulc(subc(a, mulc(y, y)), x), 0.5));
     return y;
 }
 // quad_double.hpp:372-383
@@ -947,12 +956,12 @@ XB_OP2 recip_t<r4> recip(const r4 b, int& status) {
     if (!finite(seed)) status = 2;
     r4 x = make4(seed);
 #pragma unroll 1
-    for (int it = 0; it < 2; ++it) x = add(x, mul(x, sub(make4(1.0), mul(b, x))));
+    for (int it = 0; it < 2; ++it) x = addc(x, mulc(x, subc(make4(1.0), mulc(b, x))));
     return {x};
 }
 XB_DEV r4 divide(const r4& a, const r4& b, const recip_t<r4>& rc) {
-    r4 q = mul(a, rc.x);
-    return add(q, mul(rc.x, sub(a, mul(b, q))));
+    r4 q = mulc(a, rc.x);
+    return addc(q, mulc(rc.x, subc(a, mulc(b, q))));
 }
 
 template <class R>

@@ -87,6 +87,16 @@ XB_DEVICE r4 shfl_xor_r<r4>(const r4& v, int m) {
     return {__shfl_xor_sync(0xffffffffu, v.c0, m), __shfl_xor_sync(0xffffffffu, v.c1, m),
             __shfl_xor_sync(0xffffffffu, v.c2, m), __shfl_xor_sync(0xffffffffu, v.c3, m)};
 }
+// partner exchange inside a lane pair whose lanes may run without the rest
+// of the warp: mask = the two lanes only
+XB_DEVICE r1 shfl_pair(const r1& v, unsigned mask) { return {__shfl_xor_sync(mask, v.c0, 1)}; }
+XB_DEVICE r2 shfl_pair(const r2& v, unsigned mask) {
+    return {__shfl_xor_sync(mask, v.c0, 1), __shfl_xor_sync(mask, v.c1, 1)};
+}
+XB_DEVICE r4 shfl_pair(const r4& v, unsigned mask) {
+    return {__shfl_xor_sync(mask, v.c0, 1), __shfl_xor_sync(mask, v.c1, 1),
+            __shfl_xor_sync(mask, v.c2, 1), __shfl_xor_sync(mask, v.c3, 1)};
+}
 template <class R>
 XB_DEVICE cx<R> shfl_down_c(const cx<R>& v, int o) {
     return {shfl_down_r(v.re, o), shfl_down_r(v.im, o)};

@@ -101,7 +101,7 @@ XB_DEVICE real_t<L> g2_tree(const g2<L, RPP>& g, real_t<L> acc, double* slot_loc
 #pragma unroll 1
     for (int s = 1; s < 16; s <<= 1) {
         R other = shfl_down_r(acc, 2 * s);
-        if ((pi & (2 * s - 1)) == 0 && (g.gpair + s) * RPP < g.m) acc = add(acc, other);
+        if ((pi & (2 * s - 1)) == 0 && (g.gpair + s) * RPP < g.m) acc = addc(acc, other);
     }
     // slot[buf][warp][part] : L doubles
     double* my = slot_local + ((buf * kG2Warps + g.warp) * 2) * L;
@@ -125,7 +125,7 @@ XB_DEVICE real_t<L> g2_tree(const g2<L, RPP>& g, real_t<L> acc, double* slot_loc
                 st0 = w;
                 have = 1;
             } else {
-                st0 = add(st0, w);  // in-lane level (stride 1 partial)
+                st0 = addc(st0, w);  // in-lane level (stride 1 partial)
             }
         }
     }
@@ -133,7 +133,7 @@ XB_DEVICE real_t<L> g2_tree(const g2<L, RPP>& g, real_t<L> acc, double* slot_loc
 #pragma unroll 1
     for (int s = 1; s < 16; s <<= 1) {
         R other = shfl_down_r(v, 2 * s);
-        if ((pi & (2 * s - 1)) == 0 && (pi + s) * npp * rows_pp < g.m) v = add(v, other);
+        if ((pi & (2 * s - 1)) == 0 && (pi + s) * npp * rows_pp < g.m) v = addc(v, other);
     }
     (void)have;
     return shfl_idx_r(v, g.lane & 1);  // lane 0 holds re (or the real total), lane 1 im
@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(kG2Threads, 1) mgs_grid2_kernel(GridParams p) 
         atomicMin(p.key, status_key(pos, column, code));
     };
 
+    if (p.trace && blockIdx.x == 0 && g.tid == 0) p.trace[n * 8 + 7] = g2_timer();
     // ---- copy owned columns into the workspace (AoS image); QR: zero strict lower R
     for (int j = cid; j < ncol; j += G) {
         const double* src = (j < n) ? p.a + (int64_t)j * m * L2 : p.b;
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kG2Threads, 1) mgs_grid2_kernel(GridParams p) 
 
     // ---- norm pre-pass (mgs.hpp:91-96 / :143): column_norm of every column --
     auto col_norm2 = [&](const double* c) -> R {
-        R acc = lane_tree<2, R>(g.cnt, [&](int t) {
+        R acc = lane_tree<(RPP >= 4 ? 3 : 2), R>(g.cnt, [&](int t) {
             C a = g.ld_row(c, g.row0 + t);
             return cdot_re(a, a);
         });
@@ -230,6 +231,7 @@ __global__ void __launch_bounds__(kG2Threads, 1) mgs_grid2_kernel(GridParams p) 
     }
     const bool pre_err = __ldcg(p.key) != kNoError;
     int* abortw = p.counters + 2;
+    if (p.trace && blockIdx.x == 0 && g.tid == 0) p.trace[n * 8 + 6] = g2_timer();
 
     // normalise column j (owner cluster) and publish it.  Returns false on error.
     auto normalize_publish = [&](int j) -> bool {
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(kG2Threads, 1) mgs_grid2_kernel(GridParams p) 
             // r_kj = q_k^H a_j (reduction.hpp:45-51): this lane's half of the
             // complex leaf cmul(conj(q), a) (complex.hpp:41-44), operands
             // selected so both halves run the same code
-            R acc = lane_tree<2, R>(g.cnt, [&](int t) {
+            R acc = lane_tree<(RPP >= 4 ? 3 : 2), R>(g.cnt, [&](int t) {
                 C a = g.ld_row(c, g.row0 + t);
                 const R y1 = g.part ? a.im : a.re, y2 = g.part ? a.re : a.im;
                 rpair<R> pr = mul2(q[t].re, y1, neg(q[t].im), y2);
@@ -391,16 +393,18 @@ __global__ void __launch_bounds__(kG2Threads, 1) mgs_grid2_kernel(GridParams p) 
             s_key = __ldcg(p.key);
         }
         __syncthreads();
+        if (p.trace && g.tid == 0) p.trace[n * 8 + 4] = g2_timer();
         if (LSQ && s_key == kNoError) {
             // mgs.hpp:157 -> :110-126; x in (dynamic) shared memory
             extern __shared__ double xs[];
             double* prep = p.rws + (int64_t)n * n * L2 + (int64_t)n * L2;
-            bool bad = cta_back_substitute<L>(n, p.rws, ydst, xs, prep, &s_key,
+            bool bad = pair_back_substitute<L>(n, p.rws, ydst, xs, prep, &s_key,
                                               2 + (long long)n * (ncol + 1));
             if (!bad)
                 for (int e = g.tid; e < n * L2; e += kG2Threads) p.x[e] = xs[e];
             __syncthreads();
         }
+        if (p.trace && g.tid == 0) p.trace[n * 8 + 5] = g2_timer();
         if (g.tid == 0) {
             unsigned long long key = s_key;
             xqr_status st;
@@ -460,6 +464,8 @@ cudaError_t launch_grid2(const GridParams& p, bool lsq, int max_clusters, cudaSt
                            : launch_grid2_t<L, 1, false>(p, max_clusters, s);
         case 2: return lsq ? launch_grid2_t<L, 2, true>(p, max_clusters, s)
                            : launch_grid2_t<L, 2, false>(p, max_clusters, s);
+        case 4: return lsq ? launch_grid2_t<L, 4, true>(p, max_clusters, s)
+                           : launch_grid2_t<L, 4, false>(p, max_clusters, s);
         default: return cudaErrorInvalidValue;
     }
 }
