@@ -103,6 +103,26 @@ int xqr_back_substitute_batched_device(xqr_ctx* ctx, int limbs, int64_t batch, i
                                        const double* d_r, const double* d_y, double* d_x,
                                        xqr_status* d_st);
 
+/* ---- verification metrics ------------------------------ */
+/* mgs.hpp:161-178: out (L doubles) = max_ij |a_ij - sum_{l<=j} q_il r_lj|
+ * (working precision, left-to-right sums); mgs.hpp:208-222: out = max over
+ * i <= j of |q_i^H q_j - delta_ij| on the fixed tree.  XQR_OVERFLOW if a
+ * value is not finite.  Batched forms: out has batch*L doubles. */
+int xqr_residual_max_entry(xqr_ctx* ctx, int limbs, int64_t m, int64_t n, const double* a,
+                           const double* q, const double* r, double* out, xqr_status* st);
+int xqr_orthogonality_defect(xqr_ctx* ctx, int limbs, int64_t m, int64_t n, const double* q,
+                             double* out, xqr_status* st);
+int xqr_residual_max_entry_batched(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                                   const double* a, const double* q, const double* r, double* out,
+                                   xqr_status* st);
+int xqr_orthogonality_defect_batched(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                                     const double* q, double* out, xqr_status* st);
+int xqr_residual_max_entry_batched_device(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                                          const double* d_a, const double* d_q, const double* d_r,
+                                          double* d_out, xqr_status* d_st);
+int xqr_orthogonality_defect_batched_device(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                                            const double* d_q, double* d_out, xqr_status* d_st);
+
 /* ---- synthetic inputs (host) --------------------------------------------- */
 /* The reference generator: split_mix64 (random.hpp:17-41), log-uniform
  * modulus in [10^-g, 10^g] computed in double and widened exactly

@@ -40,6 +40,8 @@ __all__ = [
     "usage_error", "cuda_error", "normalize_mode", "Context", "context", "library_path",
     "mgs_qr", "lsq_solve", "back_substitute", "par_mgs_qr", "par_lsq_solve",
     "par_back_substitute", "mgs_qr_batched", "lsq_solve_batched", "arith", "real_traits",
+    "residual_max_entry", "orthogonality_defect", "residual_max_entry_batched",
+    "orthogonality_defect_batched",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -146,6 +148,12 @@ _SIGNATURES = {
     "xqr_lsq_solve_batched_device": ([_vp, _ci, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp], _ci),
     "xqr_back_substitute_batched_device": ([_vp, _ci, _i64, _i64, _vp, _vp, _vp, _vp], _ci),
     "xqr_arith": ([_vp, _ci, _ci, _i64, _dp, _dp, _dp, ctypes.POINTER(ctypes.c_int32)], _ci),
+    "xqr_residual_max_entry": ([_vp, _ci, _i64, _i64, _dp, _dp, _dp, _dp, _sp], _ci),
+    "xqr_orthogonality_defect": ([_vp, _ci, _i64, _i64, _dp, _dp, _sp], _ci),
+    "xqr_residual_max_entry_batched": ([_vp, _ci, _i64, _i64, _i64, _dp, _dp, _dp, _dp, _sp], _ci),
+    "xqr_orthogonality_defect_batched": ([_vp, _ci, _i64, _i64, _i64, _dp, _dp, _sp], _ci),
+    "xqr_residual_max_entry_batched_device": ([_vp, _ci, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp], _ci),
+    "xqr_orthogonality_defect_batched_device": ([_vp, _ci, _i64, _i64, _i64, _vp, _vp, _vp], _ci),
     "xqr_gen_systems": ([_ci, _i64, _i64, _i64, ctypes.c_double, ctypes.c_uint64, _i64, _ci, _dp,
                          _dp], _ci),
     "xqr_ctx_launch_count": ([_vp], _i64),
@@ -310,6 +318,67 @@ def back_substitute(r, y, device: int = 0):
                                       x.ctypes.data_as(_dp), ctypes.byref(st))
     ctx.check(rc, st)
     return x
+
+
+def residual_max_entry(a, q, r, device: int = 0):
+    """mgs.hpp:161-178: max entry modulus of A - QR (working precision).
+    a, q (n, m, 2, L); r (n, n, 2, L).  Returns an (L,) array."""
+    n, m, _, L = a.shape
+    if q.shape != a.shape or r.shape != (n, n, 2, L):
+        raise dimension_error("factor shapes do not match the input matrix")
+    ctx = context(device)
+    a, pa = _f64(a)
+    q, pq = _f64(q)
+    r, pr = _f64(r)
+    out = np.zeros(L)
+    st = xqr_status()
+    rc = ctx._lib.xqr_residual_max_entry(ctx.handle, L, m, n, pa, pq, pr, out.ctypes.data_as(_dp),
+                                         ctypes.byref(st))
+    ctx.check(rc, st)
+    return out
+
+
+def orthogonality_defect(q, device: int = 0):
+    """mgs.hpp:208-222: max entry modulus of Q^H Q - I (tree inner products)."""
+    n, m, _, L = q.shape
+    ctx = context(device)
+    q, pq = _f64(q)
+    out = np.zeros(L)
+    st = xqr_status()
+    rc = ctx._lib.xqr_orthogonality_defect(ctx.handle, L, m, n, pq, out.ctypes.data_as(_dp),
+                                           ctypes.byref(st))
+    ctx.check(rc, st)
+    return out
+
+
+def residual_max_entry_batched(a, q, r, device: int = 0):
+    """Batched residual_max_entry: a, q (batch, n, m, 2, L), r (batch, n, n, 2, L);
+    returns (out (batch, L), codes)."""
+    batch, n, m, _, L = a.shape
+    ctx = context(device)
+    a, pa = _f64(a)
+    q, pq = _f64(q)
+    r, pr = _f64(r)
+    out = np.zeros((batch, L))
+    st = (xqr_status * max(batch, 1))()
+    rc = ctx._lib.xqr_residual_max_entry_batched(ctx.handle, L, batch, m, n, pa, pq, pr,
+                                                 out.ctypes.data_as(_dp), st)
+    if rc >= XQR_USAGE:
+        _raise(rc, 0, ctx.last_error())
+    return out, np.array([st[i].code for i in range(batch)], dtype=np.int32)
+
+
+def orthogonality_defect_batched(q, device: int = 0):
+    batch, n, m, _, L = q.shape
+    ctx = context(device)
+    q, pq = _f64(q)
+    out = np.zeros((batch, L))
+    st = (xqr_status * max(batch, 1))()
+    rc = ctx._lib.xqr_orthogonality_defect_batched(ctx.handle, L, batch, m, n, pq,
+                                                   out.ctypes.data_as(_dp), st)
+    if rc >= XQR_USAGE:
+        _raise(rc, 0, ctx.last_error())
+    return out, np.array([st[i].code for i in range(batch)], dtype=np.int32)
 
 
 def _check_workers(workers):

@@ -650,6 +650,90 @@ int xqr_back_substitute(xqr_ctx* ctx, int limbs, int64_t rows, int64_t cols, con
     return hs.code;
 }
 
+// ---- verification metrics (mgs.hpp:161-178, :208-222) -------------------------------
+namespace {
+int metric_device(xqr_ctx* ctx, int which, int limbs, int64_t batch, int64_t m, int64_t n,
+                  const double* d_a, const double* d_q, const double* d_r, double* d_out,
+                  xqr_status* d_st, size_t scratch_off) {
+    arena_plan plan;
+    const size_t o_part = plan.add(sizeof(double) * batch * xb::metric_blocks(which, (int)m, (int)n) * limbs);
+    const size_t o_flg = plan.add(sizeof(int) * batch);
+    cudaError_t e = ensure_arena(ctx, scratch_off + plan.total + 256);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
+    int* flags = reinterpret_cast<int*>(at(ctx, scratch_off + o_flg));
+    cudaMemsetAsync(flags, 0, sizeof(int) * batch, ctx->stream);
+    e = xb::launch_metric(limbs, which, batch, (int)m, (int)n, d_a, d_q, d_r, d_out,
+                          reinterpret_cast<double*>(at(ctx, scratch_off + o_part)), flags, d_st, ctx->stream);
+    ctx->launches += 2;
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "metric launch");
+    return 0;
+}
+
+int metric_host(xqr_ctx* ctx, int which, int limbs, int64_t batch, int64_t m, int64_t n, const double* a,
+                const double* q, const double* r, double* out, xqr_status* st) {
+    if (!ctx) return XQR_USAGE;
+    if (int c = check_shape(ctx, st, limbs, batch, m, n)) return c;
+    if (batch == 0) return 0;
+    cudaSetDevice(ctx->device);
+    const size_t L2 = 2 * (size_t)limbs;
+    const size_t a_b = which == 0 ? sizeof(double) * batch * m * n * L2 : 0;
+    const size_t q_b = sizeof(double) * batch * m * n * L2;
+    const size_t r_b = which == 0 ? sizeof(double) * batch * n * n * L2 : 0;
+    arena_plan plan;
+    const size_t o_a = plan.add(a_b), o_q = plan.add(q_b), o_r = plan.add(r_b),
+                 o_o = plan.add(sizeof(double) * batch * limbs), o_s = plan.add(sizeof(xqr_status) * batch);
+    cudaError_t e = ensure_arena(ctx, plan.total + 256);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
+    if (a_b) cudaMemcpyAsync(at(ctx, o_a), a, a_b, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(at(ctx, o_q), q, q_b, cudaMemcpyHostToDevice, ctx->stream);
+    if (r_b) cudaMemcpyAsync(at(ctx, o_r), r, r_b, cudaMemcpyHostToDevice, ctx->stream);
+    int rc = metric_device(ctx, which, limbs, batch, m, n, (const double*)at(ctx, o_a),
+                           (const double*)at(ctx, o_q), (const double*)at(ctx, o_r), (double*)at(ctx, o_o),
+                           (xqr_status*)at(ctx, o_s), plan.total);
+    if (rc) return rc;
+    std::vector<xqr_status> hst(batch);
+    cudaMemcpyAsync(out, at(ctx, o_o), sizeof(double) * batch * limbs, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(hst.data(), at(ctx, o_s), sizeof(xqr_status) * batch, cudaMemcpyDeviceToHost, ctx->stream);
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "metric");
+    if (st) std::memcpy(st, hst.data(), sizeof(xqr_status) * batch);
+    return first_code(hst);
+}
+}  // namespace
+
+int xqr_residual_max_entry(xqr_ctx* ctx, int limbs, int64_t m, int64_t n, const double* a,
+                           const double* q, const double* r, double* out, xqr_status* st) {
+    return metric_host(ctx, 0, limbs, 1, m, n, a, q, r, out, st);
+}
+int xqr_orthogonality_defect(xqr_ctx* ctx, int limbs, int64_t m, int64_t n, const double* q,
+                             double* out, xqr_status* st) {
+    return metric_host(ctx, 1, limbs, 1, m, n, nullptr, q, nullptr, out, st);
+}
+int xqr_residual_max_entry_batched(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                                   const double* a, const double* q, const double* r, double* out,
+                                   xqr_status* st) {
+    return metric_host(ctx, 0, limbs, batch, m, n, a, q, r, out, st);
+}
+int xqr_orthogonality_defect_batched(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                                     const double* q, double* out, xqr_status* st) {
+    return metric_host(ctx, 1, limbs, batch, m, n, nullptr, q, nullptr, out, st);
+}
+int xqr_residual_max_entry_batched_device(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                                          const double* d_a, const double* d_q, const double* d_r,
+                                          double* d_out, xqr_status* d_st) {
+    if (!ctx) return XQR_USAGE;
+    if (int c = check_shape(ctx, nullptr, limbs, batch, m, n)) return c;
+    cudaSetDevice(ctx->device);
+    return batch ? metric_device(ctx, 0, limbs, batch, m, n, d_a, d_q, d_r, d_out, d_st, 0) : 0;
+}
+int xqr_orthogonality_defect_batched_device(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
+                                            const double* d_q, double* d_out, xqr_status* d_st) {
+    if (!ctx) return XQR_USAGE;
+    if (int c = check_shape(ctx, nullptr, limbs, batch, m, n)) return c;
+    cudaSetDevice(ctx->device);
+    return batch ? metric_device(ctx, 1, limbs, batch, m, n, nullptr, d_q, nullptr, d_out, d_st, 0) : 0;
+}
+
 int xqr_arith(xqr_ctx* ctx, int limbs, int op, int64_t count, const double* a, const double* b,
               double* out, int32_t* codes) {
     if (!ctx) return XQR_USAGE;

@@ -108,6 +108,12 @@ cudaError_t launch_grid_L1(const GridParams& p, int grid, bool lsq, cudaStream_t
 cudaError_t launch_grid_L2(const GridParams& p, int grid, bool lsq, cudaStream_t s);
 cudaError_t launch_grid_L4(const GridParams& p, int max_clusters, bool lsq, cudaStream_t s);
 
+// verification metrics (metrics.cu): which 0 = residual_max_entry, 1 = orthogonality_defect
+int64_t metric_blocks(int which, int m, int n);
+cudaError_t launch_metric(int limbs, int which, int64_t batch, int m, int n, const double* a,
+                          const double* q, const double* r, double* out, double* part, int* flags,
+                          xqr_status* st, cudaStream_t s);
+
 cudaError_t launch_arith(int limbs, int op, int64_t count, const double* a, const double* b,
                          double* out, int32_t* codes, cudaStream_t s);
 

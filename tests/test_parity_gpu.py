@@ -257,6 +257,34 @@ def test_batched_pipeline_chunks(port, monkeypatch, pinned):
     assert codes[17] == 1 and cols[17] == 5
 
 
+@pytest.mark.parametrize("L", [1, 2, 4])
+@pytest.mark.parametrize("m,n", [(8, 8), (33, 33), (40, 7), (64, 64), (129, 20)])
+def test_metrics_bitwise(port, L, m, n):
+    """Device residual_max_entry / orthogonality_defect (mgs.hpp:161-222) ==
+    the oracle's, on a factorisation and on a perturbed one."""
+    if L == 4 and m * n > 3000:
+        pytest.skip("oracle too slow for this shape in qd")
+    a, _ = port.gen_system(L, m, n, 1.0, 31 * m + n)
+    q, r, st = port.mgs_qr(a)
+    assert st[0] == 0
+    q2 = q.copy()
+    q2[n // 2, m // 3, 0, 0] *= 1.0 + 2.0 ** -20
+    for qq in (q, q2):
+        want, wst = port.residual_max_entry(a, qq, r)
+        got = xqr.residual_max_entry(a, qq, r)
+        assert_same(got, want, "residual")
+        want, wst = port.orthogonality_defect(qq)
+        got = xqr.orthogonality_defect(qq)
+        assert_same(got, want, "defect")
+    # batched forms agree with the single-system forms
+    ab, qb, rb = np.stack([a, a]), np.stack([q, q2]), np.stack([r, r])
+    res, codes = xqr.residual_max_entry_batched(ab, qb, rb)
+    assert not codes.any()
+    assert_same(res[1], port.residual_max_entry(a, q2, r)[0], "batched residual")
+    dfc, codes = xqr.orthogonality_defect_batched(qb)
+    assert_same(dfc[1], port.orthogonality_defect(q2)[0], "batched defect")
+
+
 def test_par_api_routes_to_device(port):
     a, b = port.gen_system(2, 33, 33, 1.0, 7)
     x, z, _ = port.lsq_solve(a, b)
