@@ -182,4 +182,31 @@ lsq_batch_result<R> lsq_solve_batched(const std::vector<col_matrix<R>>& a,
     return out;
 }
 
+// mgs.hpp:161-178 -- largest entry modulus of A - QR, in working precision.
+template <class R>
+R residual_max_entry(const col_matrix<R>& a, const col_matrix<R>& q, const col_matrix<R>& r) {
+    const std::size_t m = a.rows(), n = a.cols();
+    if (q.rows() != m || q.cols() != n || r.rows() != n || r.cols() != n)
+        throw dimension_error("factor shapes do not match the input matrix");
+    std::vector<double> ai = device::pack(a), qi = device::pack(q), ri = device::pack(r);
+    R out{};
+    xqr_status st{};
+    int rc = xqr_residual_max_entry(device::context(), device::limbs<R>(), (int64_t)m, (int64_t)n,
+                                    ai.data(), qi.data(), ri.data(), reinterpret_cast<double*>(&out), &st);
+    device::raise_status(rc, st);
+    return out;
+}
+
+// mgs.hpp:208-222 -- largest entry modulus of Q^H Q - I.
+template <class R>
+R orthogonality_defect(const col_matrix<R>& q) {
+    std::vector<double> qi = device::pack(q);
+    R out{};
+    xqr_status st{};
+    int rc = xqr_orthogonality_defect(device::context(), device::limbs<R>(), (int64_t)q.rows(),
+                                      (int64_t)q.cols(), qi.data(), reinterpret_cast<double*>(&out), &st);
+    device::raise_status(rc, st);
+    return out;
+}
+
 }  // namespace xqr

@@ -41,7 +41,7 @@ __all__ = [
     "mgs_qr", "lsq_solve", "back_substitute", "par_mgs_qr", "par_lsq_solve",
     "par_back_substitute", "mgs_qr_batched", "lsq_solve_batched", "arith", "real_traits",
     "residual_max_entry", "orthogonality_defect", "residual_max_entry_batched",
-    "orthogonality_defect_batched",
+    "orthogonality_defect_batched", "accuracy_sweep", "gen_systems",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -462,6 +462,35 @@ def gen_systems(limbs: int, batch: int, m: int, n: int, g: float = 1.0, seed: in
     if rc:
         _raise(rc, what="gen_systems")
     return (a, b) if rhs else a
+
+
+def accuracy_sweep(limbs: int, m: int = 32, n: int = 32, g_values=(1.0,), trials: int = 100,
+                   seed: int = 1, device: int = 0):
+    """The reference's accuracy sweep (experiment.hpp:117-176, paper Table 2)
+    on the device: for each g (index gi), `trials` matrices drawn from
+    split_mix64(seed).split(gi*trials + t) (log-uniform modulus in
+    [10^-g, 10^g]), mgs_qr of each (batched kernel), e = residual_max_entry
+    (device metric), log10(e's leading limb); breakdowns are excluded but
+    counted.  Returns one dict per g: g, trials, exclusions, m_e = min log10 e,
+    M_e = max log10 e, D_e = m_e - M_e, log10_e (per kept trial)."""
+    out = []
+    for gi, g in enumerate(g_values):
+        a = gen_systems(limbs, trials, m, n, float(g), seed, gi * trials, rhs=False)
+        q, r, codes, _ = mgs_qr_batched(a, device=device)
+        keep = codes == 0
+        e, ecodes = residual_max_entry_batched(a[keep], q[keep], r[keep], device=device) if keep.any() \
+            else (np.zeros((0, limbs)), np.zeros(0, dtype=np.int32))
+        log10_e = np.log10(e[:, 0]) if len(e) else np.zeros(0)
+        rec = {"g": float(g), "m": m, "n": n, "limbs": limbs, "trials": int(keep.sum()),
+               "exclusions": int((~keep).sum()), "log10_e": log10_e.tolist()}
+        if len(log10_e):
+            rec["m_e"] = float(log10_e.min())
+            rec["M_e"] = float(log10_e.max())
+            rec["D_e"] = rec["m_e"] - rec["M_e"]
+        else:
+            rec["m_e"] = rec["M_e"] = rec["D_e"] = float("nan")
+        out.append(rec)
+    return out
 
 
 def arith(limbs: int, op: int, a, b=None, device: int = 0):

@@ -116,6 +116,14 @@ void random_parity(std::size_t m, std::size_t n, std::uint64_t seed) {
     auto sol = par_lsq_solve(A, B, 8);
     CHECK(std::memcmp(sol.x.data(), x.data(), x.size() * 8) == 0);
     CHECK(std::memcmp(&sol.residual_norm, z.data(), z.size() * 8) == 0);
+    // verification metrics (mgs.hpp:161-222) on the device == the oracle's
+    std::vector<double> res(L), dfc(L);
+    xo_residual_max_entry(L, (int64_t)m, (int64_t)n, a.data(), q.data(), r.data(), res.data(), &st);
+    xo_orthogonality_defect(L, (int64_t)m, (int64_t)n, q.data(), dfc.data(), &st);
+    R gres = residual_max_entry(A, f.q, f.r);
+    R gdfc = orthogonality_defect(f.q);
+    CHECK(std::memcmp(&gres, res.data(), L * 8) == 0);
+    CHECK(std::memcmp(&gdfc, dfc.data(), L * 8) == 0);
     // batched extension
     std::vector<col_matrix<R>> As(3, A);
     std::vector<cvector<R>> Bs(3, B);

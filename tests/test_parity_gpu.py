@@ -285,6 +285,27 @@ def test_metrics_bitwise(port, L, m, n):
     assert_same(dfc[1], port.orthogonality_defect(q2)[0], "batched defect")
 
 
+@pytest.mark.parametrize("L", [1, 2, 4])
+def test_accuracy_sweep_matches_reference_loop(port, L):
+    """accuracy_sweep (paper Table 2 harness, experiment.hpp:117-176) on the
+    GPU == the reference's serial loop run on the oracle, trial by trial
+    (including breakdown exclusions at large g)."""
+    g_values, trials, m = (1.0, 8.0, 150.0), 12, 10
+    recs = xqr.accuracy_sweep(L, m, m, g_values, trials, seed=20260901)
+    for gi, (g, rec) in enumerate(zip(g_values, recs)):
+        want, excl = [], 0
+        for t in range(trials):
+            a = port.gen_system(L, m, m, g, 20260901, gi * trials + t, rhs=False)
+            q, r, st = port.mgs_qr(a)
+            if st[0] == 1:
+                excl += 1
+                continue
+            e, _ = port.residual_max_entry(a, q, r)
+            want.append(np.log10(e[0]))
+        assert rec["exclusions"] == excl
+        assert np.array_equal(np.array(rec["log10_e"]), np.array(want)), g
+
+
 def test_par_api_routes_to_device(port):
     a, b = port.gen_system(2, 33, 33, 1.0, 7)
     x, z, _ = port.lsq_solve(a, b)
