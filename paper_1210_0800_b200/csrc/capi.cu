@@ -121,10 +121,13 @@ int check_shape(xqr_ctx* ctx, xqr_status* st, int limbs, int64_t batch, int64_t 
 
 // A single system large enough to feed several SMs goes to the cluster grid
 // kernel (xgrid2.cuh); small ones stay on one CTA (xmgs.cuh).
-bool use_grid_path(xqr_ctx* ctx, int m, int n) {
+bool use_grid_path(xqr_ctx* ctx, int limbs, int m, int n) {
     if (const char* e = std::getenv("XQR_FORCE_CTA")) {
         if (e[0] == '1') return false;
     }
+    // quad-double pivots are slow enough that even a small system gains from
+    // spreading its columns over SMs; double-double needs a larger one
+    if (limbs == 4) return ctx->coop && n >= 4 && m >= 16 && m <= xb::kGridMaxRows;
     return ctx->coop && n >= 8 && m >= 64 && m <= xb::kGridMaxRows;
 }
 
@@ -217,7 +220,7 @@ int solve_device(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t m, in
                  const double* d_a, const double* d_b, double* d_q, double* d_r, double* d_x,
                  double* d_z, xqr_status* d_st, size_t scratch_off, bool timed) {
     const int ncol = (int)n + (lsq ? 1 : 0);
-    if (batch == 1 && use_grid_path(ctx, (int)m, (int)n))
+    if (batch == 1 && use_grid_path(ctx, limbs, (int)m, (int)n))
         return solve_grid(ctx, lsq, limbs, (int)m, (int)n, d_a, d_b, d_q, d_r, d_x, d_z, d_st,
                           scratch_off, timed);
     xb::SolveParams p{};
