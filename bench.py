@@ -322,6 +322,11 @@ def main():
             traffic = json.load(open(tf)).get(f"cqd_{m}x{n}_batch{per_rank}")
         except Exception:
             traffic = None
+    hbm_peak = 6542.1
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
 
     single = {}
     cpu = None
@@ -330,6 +335,23 @@ def main():
             for (L, mm, nn) in ((2, 256, 256), (4, 256, 256), (4, 512, 256)):
                 single[f"{'cdd' if L == 2 else 'cqd'}_{mm}x{nn}"] = single_system_latency(
                     xqr, ctx, torch, L, mm, nn)
+            # quality-up: cqd on the GPU vs cdd on one host
+            # core (the reference itself), same A and b, n = 80
+            try:
+                import oracle  # CPU baseline leg only
+
+                ref = oracle.reference() or oracle.port()
+                gq = single_system_latency(xqr, ctx, torch, 4, 80, 80)
+                a80, b80 = xqr.gen_systems(2, 1, 80, 80, 1.0, 1, -1)
+                t0 = time.perf_counter()
+                ref.lsq_solve(a80[0], b80[0])
+                cpu_ms = 1e3 * (time.perf_counter() - t0)
+                single["quality_up_n80"] = {
+                    "gpu_cqd_us": gq["us_per_system"], "cpu_cdd_us_1core": cpu_ms * 1e3,
+                    "speedup": cpu_ms * 1e3 / gq["us_per_system"],
+                    "paper_c2050_vs_x5690": 3.08, "digits": "cqd ~62 vs cdd ~31"}
+            except Exception as exc:  # noqa: BLE001
+                single["quality_up_n80"] = {"unavailable": str(exc)}
         if not args.no_cpu:
             threads = os.cpu_count() or 1
             sample = max(threads, 16)
@@ -369,8 +391,13 @@ def main():
                          "kernel": "mgs_cta_kernel<4,3,4,true>",
                          "fp64_tflops": flops * per_rank / kernel_s / 1e12,
                          "fp64_tflops_peak": FP64_PEAK_FLOPS / 1e12,
-                         "peak_source": "measured (profiles/r01_fp64_probe.log)",
-                         "work_per_system_instr": instr, "kernel_ms": kernel_s * 1e3},
+                         "peak_source": "measured (profiles/r01_fp64_probe.log): MEASURED_PEAKS.json "
+                                        "has no FP64 entry",
+                         "work_per_system_instr": instr, "kernel_ms": kernel_s * 1e3,
+                         "secondary": {"bound": "hbm", "unit": "GB/s", "peak": hbm_peak,
+                                       "achieved": (traffic / kernel_s / 1e9) if traffic else None,
+                                       "frac": (traffic / kernel_s / 1e9 / hbm_peak) if traffic else None,
+                                       "note": "ncu dram bytes of the same launch; HBM is not the bound"}},
             "clocks": clk,
             "status": {"failed_systems": n_fail, "bitwise_vs_reference_streams_0_3": parity},
             "single_system": single,
