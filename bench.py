@@ -227,9 +227,10 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1210_0800_b200.sharding import max_over_ranks, shard
+
     limbs, m, n = 4, args.m, args.n
-    per_rank = args.batch if args.scaling == "weak" else args.batch // world
-    first = rank * per_rank
+    first, per_rank = shard(args.batch, rank, world, args.scaling)
 
     ctx = xqr.Context(local)
     # one explicit stream shared by torch (events, copies) and the C ABI
@@ -271,11 +272,8 @@ def main():
     launches = ctx.launch_count - launches0
     ms = e0.elapsed_time(e1)
     last_kernel_ms = ctx.last_kernel_ms  # CUDA events around the last launch, ctx stream
-    if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    total = per_rank * world * args.steps
+    ms = max_over_ranks(ms, dist, "cuda")
+    total = (args.batch * world if args.scaling == "weak" else args.batch) * args.steps
     value = total / (ms / 1e3)
 
     codes = dst.cpu().numpy()[:, 0] & 0xFFFFFFFF
@@ -304,11 +302,8 @@ def main():
         xh, zh, ch, _ = xqr.lsq_solve_batched(a_pin, b_pin, device=local)
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-    if dist:
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = per_rank * world / e2e_s
+    e2e_s = max_over_ranks(e2e_s, dist, "cuda")
+    e2e_value = (args.batch * world if args.scaling == "weak" else args.batch) / e2e_s
     h2d = a.nbytes + b.nbytes
     d2h = xh.nbytes + zh.nbytes + 16 * per_rank
 
