@@ -112,6 +112,25 @@ XB_DEV void two_prod(double a, double b, double& p, double& e) {
     e = dfma(a, b, -p);
 }
 
+// select without a branch (selp on the device: nvcc otherwise turns chains
+// of data-dependent ternaries into divergent branch ladders).  Enabled for
+// the latency-bound single-system kernels (XB_USE_SELP); the throughput-bound
+// batched kernel schedules better with plain ternaries.
+#ifndef XB_USE_SELP
+#define XB_USE_SELP 0
+#endif
+XB_DEV double dsel(bool p, double a, double b) {
+#if defined(__CUDA_ARCH__) && XB_USE_SELP
+    double r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+        : "=d"(r)
+        : "d"(a), "d"(b), "r"((int)p));
+    return r;
+#else
+    return p ? a : b;
+#endif
+}
+
 XB_DEV bool finite(double x) {
     return (dbits(x) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;
 }
@@ -448,12 +467,12 @@ XB_DEV void qadd_step(double& u, double& v, double s, int& k, double& x0, double
     two_sum(u, t, uu, ue);
     const bool zb = (te != 0.0);
     const bool emit = (ue != 0.0) && zb;
-    v = zb ? te : ue;
-    u = emit ? ue : uu;
-    x0 = (emit && k == 0) ? uu : x0;
-    if (KMAX >= 1) x1 = (emit && k == 1) ? uu : x1;
-    if (KMAX >= 2) x2 = (emit && k == 2) ? uu : x2;
-    if (KMAX >= 3) x3 = (emit && k == 3) ? uu : x3;
+    v = dsel(zb, te, ue);
+    u = dsel(emit, ue, uu);
+    x0 = dsel(emit && k == 0, uu, x0);
+    if (KMAX >= 1) x1 = dsel(emit && k == 1, uu, x1);
+    if (KMAX >= 2) x2 = dsel(emit && k == 2, uu, x2);
+    if (KMAX >= 3) x3 = dsel(emit && k == 3, uu, x3);
     k += emit ? 1 : 0;
 }
 
@@ -563,10 +582,10 @@ XB_DEV void qadd_run(qadd_st& q) {
 XB_DEV r4 qadd_finish(qadd_st& q, bool& okr) {
     // loop exit with everything consumed: x[k] = u; if (k < 3) x[k + 1] = v
     const int k = q.k;
-    const double x0 = (k == 0) ? q.u : q.x0;
-    const double x1 = (k == 1) ? q.u : ((k == 0) ? q.v : q.x1);
-    const double x2 = (k == 2) ? q.u : ((k == 1) ? q.v : q.x2);
-    const double x3 = (k == 3) ? q.u : ((k == 2) ? q.v : q.x3);
+    const double x0 = dsel(k == 0, q.u, q.x0);
+    const double x1 = dsel(k == 1, q.u, dsel(k == 0, q.v, q.x1));
+    const double x2 = dsel(k == 2, q.u, dsel(k == 1, q.v, q.x2));
+    const double x3 = dsel(k == 3, q.u, dsel(k == 2, q.v, q.x3));
     double y0 = x0, y1 = x1, y2 = x2, y3 = x3;
     bool okn;
     renorm4_fast(y0, y1, y2, y3, okn);
