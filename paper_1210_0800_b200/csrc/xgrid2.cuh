@@ -294,9 +294,12 @@ __global__ void __launch_bounds__(kG2Threads, 1) mgs_grid2_kernel(GridParams p) 
         // word), the cluster barrier hands the verdict to every CTA
         if (g.crank == 0 && g.tid == 0) {
             int v;
-            while ((v = g2_ld_acquire(p.flags + k)) < g.cs && g2_ld_acquire(abortw) == 0) {
-            }
-            s_flag = (v >= g.cs && g2_ld_acquire(abortw) == 0) ? 1 : 0;
+            // back off while waiting: dozens of clusters polling the L2 flat
+            // out slow down everyone's loads, the critical path first
+            while ((v = *(volatile int*)(p.flags + k)) < g.cs && *(volatile int*)abortw == 0)
+                __nanosleep(200);
+            __threadfence();  // acquire side (pairs with the publisher's red.release)
+            s_flag = (v >= g.cs && *(volatile int*)abortw == 0) ? 1 : 0;
         }
         cg::this_cluster().sync();
         if (*cg::this_cluster().map_shared_rank(&s_flag, 0) == 0) {
