@@ -190,6 +190,40 @@ class Oracle:
         return out, codes
 
 
+REF_IO_TOOL = os.path.join(HERE, "_ref", "ref_io_tool")
+
+
+class RefIO:
+    """The reference's own matrix_io / shortest (oracle/ref_io_tool.cpp, run as
+    a subprocess), for the file-format tests.  Reference build only."""
+
+    def _run(self, args, data: bytes) -> bytes:
+        return subprocess.run([REF_IO_TOOL] + args, input=data, capture_output=True, check=True).stdout
+
+    def write_matrix(self, a) -> str:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        n, m, _, L = a.shape
+        return self._run(["write", str(L), str(m), str(n)], a.tobytes()).decode()
+
+    def read_matrix(self, text: str):
+        """(array, limbs) or raises ValueError(line)."""
+        out = self._run(["read"], text.encode())
+        head, _, body = out.partition(b"\n")
+        tok = head.split()
+        if tok[0] == b"error":
+            raise ValueError(int(tok[1]))
+        m, n, L = int(tok[1]), int(tok[2]), int(tok[3])
+        return np.frombuffer(body, dtype=np.float64).reshape(n, m, 2, L).copy(), L
+
+    def shortest_many(self, vals):
+        out = self._run(["shortest"], np.asarray(vals, dtype=np.float64).tobytes())
+        return out.decode().split("\n")[: len(vals)]
+
+
+def ref_io() -> RefIO | None:
+    return RefIO() if os.path.exists(REF_IO_TOOL) else None
+
+
 def port() -> Oracle:
     return Oracle("port")
 
