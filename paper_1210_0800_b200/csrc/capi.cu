@@ -189,7 +189,9 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     cudaMemsetAsync(p.flags, 0, sizeof(int) * ((size_t)n + 4), ctx->stream);
     cudaMemsetAsync(p.key, 0xFF, sizeof(unsigned long long), ctx->stream);
     if (p.trace) cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * 8 * (size_t)(n + 1), ctx->stream);
-    const int max_clusters = ctx->num_sms / p.cs;
+    int per_sm = limbs == 4 ? xb::kGrid2PerSM : 1;
+    if (const char* e = std::getenv("XQR_GRID_PER_SM")) per_sm = std::max(1, std::atoi(e));  // dev
+    const int max_clusters = per_sm * ctx->num_sms / p.cs;
     if (timed) cudaEventRecord(ctx->ev0, ctx->stream);
     switch (limbs) {
         case 1: e = xb::launch_grid_L1(p, std::min(ncol, ctx->num_sms), lsq, ctx->stream); break;

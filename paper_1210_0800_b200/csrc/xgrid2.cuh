@@ -11,7 +11,9 @@
 //     lane the imaginary part of every complex quantity (the two halves of a
 //     complex multiply / add / divide are independent -- complex.hpp:26-65);
 //   * a column belongs to a thread-block CLUSTER of CS CTAs (CS = 4 for
-//     m = 256): 4 warps per CTA, one per SM sub-partition, 16 rows per warp;
+//     m = 256 and 512): 4 warps per CTA, 16 lane pairs per warp; two CTAs
+//     (of different clusters) share an SM, so one cluster's latency-bound
+//     chains fill the other's issue gaps;
 //   * the fixed reduction tree (reduction.hpp:34-40) runs in-lane (rows of a
 //     pair), then over lane pairs by shuffles, then over the cluster's warp
 //     partials read through distributed shared memory -- the same pairing as
@@ -26,6 +28,7 @@
 // re limbs then im limbs), so the loads of a lane pair are contiguous.
 #pragma once
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "xbacksub.cuh"
 #include "xcolumn.cuh"
@@ -140,7 +143,7 @@ XB_DEVICE real_t<L> g2_tree(const g2<L, RPP>& g, real_t<L> acc, double* slot_loc
 }
 
 template <int L, int RPP, bool LSQ>
-__global__ void __launch_bounds__(kG2Threads, 1) mgs_grid2_kernel(GridParams p) {
+__global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) {
     namespace cg = cooperative_groups;
     using R = real_t<L>;
     using C = cx<R>;
@@ -434,7 +437,13 @@ cudaError_t launch_grid2_t(const GridParams& p, int max_clusters, cudaStream_t s
     // x of the back substitution lives here (CTA 0); the size also keeps the
     // kernel at ONE CTA per SM, so each warp has an SM sub-partition to itself
     cfg.dynamicSmemBytes = sizeof(double) * (size_t)p.n * 2 * L;
-    if (cfg.dynamicSmemBytes < 120 * 1024) cfg.dynamicSmemBytes = 120 * 1024;
+    {
+        // CTAs per SM (kGrid2PerSM; XQR_GRID_PER_SM overrides, dev only)
+        const char* e = std::getenv("XQR_GRID_PER_SM");
+        const int per_sm = e ? std::max(1, std::atoi(e)) : kGrid2PerSM;
+        const size_t floor_b = per_sm == 1 ? 120 * 1024 : (per_sm == 2 ? 100 * 1024 : 60 * 1024);
+        if (cfg.dynamicSmemBytes < floor_b) cfg.dynamicSmemBytes = floor_b;
+    }
     if (cfg.dynamicSmemBytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)cfg.dynamicSmemBytes);

@@ -90,11 +90,13 @@ struct GridParams {
 };
 
 constexpr int kGridMaxRows = 1024;
-// quad-double (xgrid2.cuh): CTAs per cluster and rows per lane pair
+// quad-double (xgrid2.cuh): CTAs per cluster and rows per lane pair.  Two
+// CTAs share each SM; 4-CTA clusters measured best for m = 256 and 512.
+constexpr int kGrid2PerSM = 2;
 inline void grid_shape(int m, int& cs, int& rpp) {
     const int need = (m + 63) / 64;
     cs = 1;
-    while (cs < need && cs < 8) cs <<= 1;
+    while (cs < need && cs < 4) cs <<= 1;
     rpp = 1;
     while (cs * 64 * rpp < m) rpp <<= 1;
 }
