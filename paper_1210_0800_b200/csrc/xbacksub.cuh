@@ -282,6 +282,14 @@ XB_DEVICE bool pair_back_substitute(int n, const double* r, const double* y, dou
             }
             store_real<L>(xs_part(j, part), 1, v);
         }
+        // R is known from the start: pull next step's r_{j,k-1} (and the
+        // next pivot's Smith record) into L1 while the barrier drains
+        if (k >= 2) {
+            const double* rn = r + (size_t)(k - 1) * n * 2 * L;
+            for (int jj = pair; jj < k - 1; jj += P)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(rn + (size_t)jj * 2 * L + part * L));
+            if (tid == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(prep + (size_t)(k - 2) * (3 * L + 1)));
+        }
         if (__syncthreads_or(err)) return true;
     }
     return false;

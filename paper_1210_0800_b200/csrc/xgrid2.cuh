@@ -386,39 +386,52 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
     }
     // no CTA may exit while a cluster peer can still read its shared memory
     cg::this_cluster().sync();
-    // everyone done -> CTA 0 runs the fused back substitution
+    // the status so far; a least-squares solve continues in
+    // grid2_backsub_kernel (same stream) with more threads than a CTA here
     __syncthreads();
     if (g.tid == 0) {
         __threadfence();
         g2_red_release(p.counters + 1, 1);
     }
-    if (blockIdx.x == 0) {
-        __shared__ unsigned long long s_key;
-        if (g.tid == 0) {
-            while (g2_ld_acquire(p.counters + 1) < (int)gridDim.x) __nanosleep(64);
-            s_key = __ldcg(p.key);
-        }
-        __syncthreads();
-        if (p.trace && g.tid == 0) p.trace[n * 8 + 4] = g2_timer();
-        if (LSQ && s_key == kNoError) {
-            // mgs.hpp:157 -> :110-126; x in (dynamic) shared memory
-            extern __shared__ double xs[];
-            double* prep = p.rws + (int64_t)n * n * L2 + (int64_t)n * L2;
-            bool bad = pair_back_substitute<L>(n, p.rws, ydst, xs, prep, &s_key,
-                                              2 + (long long)n * (ncol + 1));
-            if (!bad)
-                for (int e = g.tid; e < n * L2; e += kG2Threads) p.x[e] = xs[e];
-            __syncthreads();
-        }
-        if (p.trace && g.tid == 0) p.trace[n * 8 + 5] = g2_timer();
-        if (g.tid == 0) {
-            unsigned long long key = s_key;
-            xqr_status st;
-            st.system = 0;
-            st.code = key == kNoError ? 0 : (int)(key & 15);
-            st.column = key == kNoError ? 0 : (int)((key >> 4) & 0xFFFFF);
-            *p.st = st;
-        }
+    if (blockIdx.x == 0 && g.tid == 0) {
+        while (g2_ld_acquire(p.counters + 1) < (int)gridDim.x) __nanosleep(64);
+        const unsigned long long key = __ldcg(p.key);
+        if (p.trace) p.trace[n * 8 + 4] = g2_timer();
+        xqr_status st;
+        st.system = 0;
+        st.code = key == kNoError ? 0 : (int)(key & 15);
+        st.column = key == kNoError ? 0 : (int)((key >> 4) & 0xFFFFF);
+        *p.st = st;
+    }
+}
+
+// Back substitution of the single-system least-squares solve (mgs.hpp:157 ->
+// :110-126): one CTA of kG2BsThreads threads = one lane pair per unknown for
+// n <= 256, so the lane that divides x_{k-1} has no other update in its step.
+constexpr int kG2BsThreads = 512;
+template <int L>
+__global__ void __launch_bounds__(kG2BsThreads, 1) grid2_backsub_kernel(GridParams p) {
+    constexpr int L2 = 2 * L;
+    extern __shared__ double xs[];
+    __shared__ unsigned long long s_key;
+    const int n = p.n, ncol = n + 1;
+    if (threadIdx.x == 0) s_key = *p.key;
+    __syncthreads();
+    if (s_key != kNoError) return;  // status already written by the factorisation
+    if (p.trace && threadIdx.x == 0) p.trace[n * 8 + 5] = g2_timer();
+    double* ydst = p.rws + (int64_t)n * n * L2;
+    double* prep = ydst + (int64_t)n * L2;
+    bool bad = pair_back_substitute<L>(n, p.rws, ydst, xs, prep, &s_key, 2 + (long long)n * (ncol + 1));
+    if (!bad)
+        for (int e = threadIdx.x; e < n * L2; e += blockDim.x) p.x[e] = xs[e];
+    __syncthreads();
+    if (p.trace && threadIdx.x == 0) p.trace[n * 8 + 6] = g2_timer();
+    if (threadIdx.x == 0 && s_key != kNoError) {
+        xqr_status st;
+        st.system = 0;
+        st.code = (int)(s_key & 15);
+        st.column = (int)((s_key >> 4) & 0xFFFFF);
+        *p.st = st;
     }
 }
 
@@ -466,7 +479,16 @@ cudaError_t launch_grid2_t(const GridParams& p, int max_clusters, cudaStream_t s
     if (nclusters > ncol) nclusters = ncol;
     if (nclusters < 1) return cudaErrorInvalidConfiguration;
     cfg.gridDim = dim3(nclusters * p.cs, 1, 1);
-    return cudaLaunchKernelEx(&cfg, kern, p);
+    e = cudaLaunchKernelEx(&cfg, kern, p);
+    if (e != cudaSuccess || !LSQ) return e;
+    auto bs = grid2_backsub_kernel<L>;
+    const size_t bsmem = sizeof(double) * (size_t)p.n * 2 * L;
+    if (bsmem > 48 * 1024) {
+        e = cudaFuncSetAttribute(bs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+        if (e != cudaSuccess) return e;
+    }
+    bs<<<1, kG2BsThreads, bsmem, s>>>(p);
+    return cudaGetLastError();
 }
 
 template <int L>
