@@ -553,6 +553,10 @@ struct qadd_st {
     double u, v, x0, x1, x2, x3;
     int k;
     bool ok;
+    // the merged order of any leftovers equals the reference's leftover fold
+    // (a's remaining limbs, then b's): an early loop exit (k == 4) is then
+    // handled in place -- the remaining limbs are added to x[3] in order
+    bool tail = false;
 };
 XB_DEV void qadd_setup(const r4& a, const r4& b, qadd_st& q) {
     const bool f0 = dabs(a.c0) > dabs(b.c0), f1 = dabs(a.c1) > dabs(b.c1);
@@ -576,7 +580,11 @@ template <int STEP>
 XB_DEV void qadd_run(qadd_st& q) {
     const double s = STEP == 0 ? q.m2 : STEP == 1 ? q.m3 : STEP == 2 ? q.m4 : STEP == 3 ? q.m5
                    : STEP == 4 ? q.m6 : q.m7;
-    if (STEP == 5) q.ok = q.ok && (q.k <= 3);  // the loop reaches its last step
+    if (q.tail && STEP >= 3 && q.k >= 4) {  // loop already left: fold (quad_double.hpp:254-255)
+        q.x3 = dadd(q.x3, s);
+        return;
+    }
+    if (STEP == 5 && !q.tail) q.ok = q.ok && (q.k <= 3);  // the loop reaches its last step
     qadd_step<(STEP < 3 ? STEP : 3)>(q.u, q.v, s, q.k, q.x0, q.x1, q.x2, q.x3);
 }
 XB_DEV r4 qadd_finish(qadd_st& q, bool& okr) {
@@ -635,6 +643,43 @@ XB_DEV void add_fast2(const r4& a1, const r4& b1, const r4& a2, const r4& b2, r4
 //                   correction, a zero operand.
 // Each pattern is recognised by exactly the comparisons the reference merge
 // makes; the merge steps are then the same six fixed steps.
+// Shifted merges: one operand leads by S levels (a Newton correction whose
+// head sits S limbs down, PAPER-style x + 0.5*x*(1 - a*x*x)):
+//   H0 .. H_{S-1}, then level pairs (H_{S+l}, T_l), then T_{4-S} .. T_3.
+// Recognised by strict separations that imply every comparison the reference
+// merge makes (|H_i| > |T_0| for the lead, pair levels apart, the lead's last
+// limb beating T's next one); the pair order is the reference rule (a first
+// iff |a| > |b|).  Fills m[0..7] and returns whether the pattern holds.
+template <int S>
+XB_DEV bool shift_merge(const r4& H, const r4& T, bool h_is_a, double (&m)[8]) {
+    const double h[4] = {H.c0, H.c1, H.c2, H.c3}, t[4] = {T.c0, T.c1, T.c2, T.c3};
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+        ok = ok && (dabs(h[i]) > dabs(t[0]));
+        m[i] = h[i];
+    }
+    double lo_prev = 0.0;
+#pragma unroll
+    for (int l = 0; l + S < 4; ++l) {
+        const double hh = h[S + l], tt = t[l];
+        // a first iff |a| > |b|
+        const bool hfirst = h_is_a ? (dabs(hh) > dabs(tt)) : !(dabs(tt) > dabs(hh));
+        const double hi = hfirst ? hh : tt, lo = hfirst ? tt : hh;
+        if (l > 0) ok = ok && (dabs(lo_prev) > dabs(hi));
+        m[S + 2 * l] = hi;
+        m[S + 2 * l + 1] = lo;
+        lo_prev = lo;
+        if (l + S == 3) {
+            // after the last pair: if T's limb went first, H_3 must beat T_{4-S}
+            ok = ok && (hfirst || (dabs(hh) > dabs(t[4 - S])));
+        }
+    }
+#pragma unroll
+    for (int l = 4 - S; l < 4; ++l) m[4 + l] = t[l];
+    return ok;
+}
+
 XB_DEV r4 add_alt_fast(const r4& a, const r4& b, bool& okr) {
     const double A0 = dabs(a.c0), A1 = dabs(a.c1), A2 = dabs(a.c2), A3 = dabs(a.c3);
     const double B0 = dabs(b.c0), B1 = dabs(b.c1), B2 = dabs(b.c2), B3 = dabs(b.c3);
@@ -669,6 +714,28 @@ XB_DEV r4 add_alt_fast(const r4& a, const r4& b, bool& okr) {
         q.m7 = pa ? a.c3 : b.c3;
     }
     q.ok = da || db || pa || pb;
+    q.tail = da;  // a0..a3 then b0..b3: leftovers come a's first, then b's
+    if (!q.ok) {
+        // shifted merges, a or b leading by 1..3 levels
+        double mm[8];
+        const bool alead = f0;
+        const r4& H = alead ? a : b;
+        const r4& T = alead ? b : a;
+        bool hit = shift_merge<2>(H, T, alead, mm);
+        if (!hit) hit = shift_merge<1>(H, T, alead, mm);
+        if (!hit) hit = shift_merge<3>(H, T, alead, mm);
+        if (hit) {
+            m0 = mm[0];
+            m1 = mm[1];
+            q.m2 = mm[2];
+            q.m3 = mm[3];
+            q.m4 = mm[4];
+            q.m5 = mm[5];
+            q.m6 = mm[6];
+            q.m7 = mm[7];
+            q.ok = true;
+        }
+    }
     quick_two_sum(m0, m1, q.u, q.v);
     q.x0 = q.x1 = q.x2 = q.x3 = 0.0;
     q.k = 0;
