@@ -1080,7 +1080,9 @@ template <class R>
 XB_DEV rpair<R> mul2(const R& a1, const R& b1, const R& a2, const R& b2) {
     return {mul(a1, b1), mul(a2, b2)};
 }
-#if !(XB_CALLS & 4)
+#if !(XB_CALLS & 4) || (XB_CALLS & 8)
+// XB_CALLS bit 8: the two adds of a complex add / subtract / product still
+// run in lockstep inline when the real operations are calls
 template <>
 XB_DEV rpair<r4> add2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2) {
     bool k1, k2;
@@ -1092,6 +1094,8 @@ XB_DEV rpair<r4> add2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2
     }
     return o;
 }
+#endif
+#if !(XB_CALLS & 4)
 template <>
 XB_DEV rpair<r4> mul2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2) {
     bool k1, k2;

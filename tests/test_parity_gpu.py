@@ -171,6 +171,43 @@ def test_overflow_reported(port, L):
         xqr.mgs_qr(a)
 
 
+@pytest.mark.parametrize("L", [2, 4])
+@pytest.mark.parametrize("m,n", [(70, 20), (24, 12)])
+def test_single_system_grid_error_paths(port, L, m, n):
+    """The whole-GPU single-system kernels (xgrid1 for dd, m >= 64; xgrid2 for
+    qd, m >= 16) report the reference's first error: a breakdown in the middle
+    of the factorisation, an overflow, and wide-range data (g = 16)."""
+    def check(call_port, call_dev, *args):
+        want = call_port(*args)
+        st = want[-1]
+        if st[0] == 0:
+            got = call_dev(*args)
+            for g, w in zip(got, want[:-1]):
+                assert_same(g, w)
+        elif st[0] == 1:
+            with pytest.raises(xqr.breakdown_error) as e:
+                call_dev(*args)
+            assert e.value.column == st[1]
+        else:
+            with pytest.raises({2: xqr.overflow_error, 3: xqr.domain_error}[st[0]]):
+                call_dev(*args)
+        return st
+
+    a, b = port.gen_system(L, m, n, 1.0, 404 + m)
+    a[n // 2] = a[1]  # dependent column
+    assert check(port.mgs_qr, xqr.mgs_qr, a)[0] == 1
+    assert check(port.lsq_solve, xqr.lsq_solve, a, b)[0] == 1
+    a, b = port.gen_system(L, m, n, 1.0, 405 + m)
+    a[n - 2, :, 0, 0] *= 1e300  # overflow inside the sweep
+    a[n - 2, :, 1, 0] *= 1e300
+    assert check(port.mgs_qr, xqr.mgs_qr, a)[0] == 2
+    assert check(port.lsq_solve, xqr.lsq_solve, a, b)[0] == 2
+    for seed in range(3):
+        a, b = port.gen_system(L, m, n, 16.0, 900 + seed)
+        check(port.mgs_qr, xqr.mgs_qr, a)
+        check(port.lsq_solve, xqr.lsq_solve, a, b)
+
+
 @pytest.mark.parametrize("L", [1, 2, 4])
 def test_back_substitute_api(port, L):
     rng = np.random.default_rng(L)
