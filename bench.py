@@ -108,6 +108,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
+def arm_config(args, world, per_rank):
+    """The `config` both arms report (ours and --impl reference)."""
+    return {"workload": f"configs[4]: batched independent cqd {args.m}x{args.n} lsq_solve "
+                        "(MGS on [A b] + back substitution)",
+            "systems_per_gpu": per_rank, "limbs": 4, "m": args.m, "n": args.n,
+            "generator": "experiment.hpp:64-79, g=1, split_mix64(1).split(rank*batch+s)",
+            "l2": "inputs (9.6 GB/GPU working set) larger than L2; no flush",
+            "parallelism": f"batch-sharded x{world}, no collective"}
+
+
 # ---- the reference arm: the reference CPU implementation on this host ---------------
 def cpu_reference_rate(limbs, m, n, sample, threads, seed=1, first_stream=0):
     """Reference lsq_solve (oracle/_ref = the unmodified reference headers
@@ -154,8 +164,8 @@ def run_reference_arm(args, rank, world):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sample / value, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64 (complex quad-double)", "data": "synthetic",
-        "config": {"workload": f"cqd {args.m}x{args.n} lsq_solve batch (configs[4])",
-                   "systems_per_step": sample, "limbs": 4, "m": args.m, "n": args.n},
+        "config": dict(arm_config(args, world, args.batch),
+                       reference_sample=f"{sample} systems per step (bounded CPU sample)"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{sample} systems per step, sequential lsq_solve per system on "
                                    f"{threads} threads"},
@@ -366,12 +376,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64 (complex quad-double, 4 limbs)", "data": "synthetic",
-            "config": {"workload": f"configs[4]: batched independent cqd {m}x{n} lsq_solve "
-                                   "(MGS on [A b] + back substitution)",
-                       "systems_per_gpu": per_rank, "limbs": limbs, "m": m, "n": n,
-                       "generator": "experiment.hpp:64-79, g=1, split_mix64(1).split(rank*batch+s)",
-                       "l2": "inputs (9.6 GB/GPU working set) larger than L2; no flush",
-                       "parallelism": f"batch-sharded x{world}, no collective"},
+            "config": arm_config(args, world, per_rank),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
                     "d2h_bytes_per_step": int(d2h * world),
                     "api": "xqr_lsq_solve_batched (pinned host A, b -> host x, z, status; "
