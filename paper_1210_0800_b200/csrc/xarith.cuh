@@ -954,6 +954,18 @@ XB_OP4 r4 mul(const r4 a, const r4 b) {
 // chains (Newton iterations, reduction trees, pivot divisions): one shared
 // copy of each operation stays hot in the instruction cache of a lone warp.
 XB_CALL_IF r4 addc(const r4 a, const r4 b) { return add(a, b); }
+// the Newton sites where the operands are known to merge unevenly (a
+// constant 1.0 or seed with zero lower limbs, a correction several limbs
+// down): try the alternative fixed merges first
+XB_CALL_IF r4 addz(const r4 a, const r4 b) {
+    bool ok;
+    r4 r = add_alt_fast(a, b, ok);
+    if (ok) return r;
+    r = add_fast(a, b, ok);
+    if (ok) return r;
+    return add_merge_pred(a, b);
+}
+XB_DEV r4 subz(const r4& a, const r4& b) { return addz(a, neg(b)); }
 XB_CALL_IF r4 mulc(const r4 a, const r4 b) { return mul(a, b); }
 XB_DEV r4 subc(const r4& a, const r4& b) { return addc(a, neg(b)); }
 XB_DEV r1 addc(const r1& a, const r1& b) { return add(a, b); }
@@ -969,10 +981,10 @@ XB_OP2 r4 rsqrt_ref(const r4 a) {
 #pragma unroll 1
     for (int it = 0; it < 2; ++it) {
         r4 t = mulc(a, x);
-        x = addc(x, mul_pwr2(mulc(x, subc(make4(1.0), mulc(t, x))), 0.5));
+        x = addz(x, mul_pwr2(mulc(x, subz(make4(1.0), mulc(t, x))), 0.5));
     }
     r4 y = mulc(a, x);
-    y = addc(y, mul_pwr2(mulc(subc(a, mulc(y, y)), x), 0.5));
+    y = addz(y, mul_pwr2(mulc(subc(a, mulc(y, y)), x), 0.5));
     return y;
 }
 // quad_double.hpp:372-383
@@ -1042,12 +1054,12 @@ XB_OP2 recip_t<r4> recip(const r4 b, int& status) {
     if (!finite(seed)) status = 2;
     r4 x = make4(seed);
 #pragma unroll 1
-    for (int it = 0; it < 2; ++it) x = addc(x, mulc(x, subc(make4(1.0), mulc(b, x))));
+    for (int it = 0; it < 2; ++it) x = addz(x, mulc(x, subz(make4(1.0), mulc(b, x))));
     return {x};
 }
 XB_DEV r4 divide(const r4& a, const r4& b, const recip_t<r4>& rc) {
     r4 q = mulc(a, rc.x);
-    return addc(q, mulc(rc.x, subc(a, mulc(b, q))));
+    return addz(q, mulc(rc.x, subc(a, mulc(b, q))));
 }
 
 template <class R>
@@ -1080,11 +1092,16 @@ template <class R>
 XB_DEV rpair<R> mul2(const R& a1, const R& b1, const R& a2, const R& b2) {
     return {mul(a1, b1), mul(a2, b2)};
 }
-#if !(XB_CALLS & 4) || (XB_CALLS & 8)
-// XB_CALLS bit 8: the two adds of a complex add / subtract / product still
-// run in lockstep inline when the real operations are calls
-template <>
-XB_DEV rpair<r4> add2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2) {
+// Two independent qd adds / products in lockstep (their dependency chains
+// interleave).  XB_CALLS bit 16 makes each pair ONE real call -- a single
+// shared copy of the lockstep code: the interleaving of the inlined form at
+// the instruction-cache cost of a call (the batched kernel's trade-off).
+#if (XB_CALLS & 16)
+#define XB_PAIR XB_CALL_IF
+#else
+#define XB_PAIR XB_DEV
+#endif
+XB_PAIR rpair<r4> add2_r4(const r4 a1, const r4 b1, const r4 a2, const r4 b2) {
     bool k1, k2;
     rpair<r4> o;
     add_fast2(a1, b1, a2, b2, o.x, k1, o.y, k2);
@@ -1094,10 +1111,7 @@ XB_DEV rpair<r4> add2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2
     }
     return o;
 }
-#endif
-#if !(XB_CALLS & 4)
-template <>
-XB_DEV rpair<r4> mul2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2) {
+XB_PAIR rpair<r4> mul2_r4(const r4 a1, const r4 b1, const r4 a2, const r4 b2) {
     bool k1, k2;
     rpair<r4> o;
     mul_fast2(a1, b1, a2, b2, o.x, k1, o.y, k2);
@@ -1106,6 +1120,17 @@ XB_DEV rpair<r4> mul2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2
         if (!k2) o.y = mul_general(a2, b2);
     }
     return o;
+}
+#if !(XB_CALLS & 4) || (XB_CALLS & 8) || (XB_CALLS & 16)
+template <>
+XB_DEV rpair<r4> add2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2) {
+    return add2_r4(a1, b1, a2, b2);
+}
+#endif
+#if !(XB_CALLS & 4) || (XB_CALLS & 16)
+template <>
+XB_DEV rpair<r4> mul2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2) {
+    return mul2_r4(a1, b1, a2, b2);
 }
 #endif
 

@@ -242,19 +242,37 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
         R s = col_norm2(c);
         const bool tr = p.trace && g.tid == 0 && g.crank == 0;
         if (tr) p.trace[j * 8 + 4] = g2_timer();
-        R rkk = rsqrt_ref(s);
-        if (tr) p.trace[j * 8 + 5] = g2_timer();
-        int code = 0;
-        if (!finite(head(s)) || !finite(head(rkk)))
-            code = XQR_OVERFLOW;
-        else if (le(rkk, thr))
-            code = XQR_BREAKDOWN;
-        recip_t<R> rc;
-        if (!code) {
-            int stc = 0;
-            rc = recip(rkk, stc);
-            code = stc;
+        // the scalar chain (sqrt, breakdown test, reciprocal) runs in warp 0
+        // only; the other warps wait and leave their issue slots to the CTA
+        // that shares the SM
+        __shared__ double s_rkk[L], s_rc[L];
+        __shared__ int s_code;
+        if (g.warp == 0) {
+            R rkk0 = rsqrt_ref(s);
+            if (tr) p.trace[j * 8 + 5] = g2_timer();
+            int code0 = 0;
+            if (!finite(head(s)) || !finite(head(rkk0)))
+                code0 = XQR_OVERFLOW;
+            else if (le(rkk0, thr))
+                code0 = XQR_BREAKDOWN;
+            recip_t<R> rc0;
+            if (!code0) {
+                int stc = 0;
+                rc0 = recip(rkk0, stc);
+                code0 = stc;
+            }
+            if (g.lane == 0) {
+                store_real<L>(s_rkk, 1, rkk0);
+                if (!code0) store_real<L>(s_rc, 1, rc0.x);
+                s_code = code0;
+            }
         }
+        __syncthreads();
+        R rkk;
+        load_real<L>(s_rkk, 1, rkk);
+        const int code = s_code;
+        recip_t<R> rc;
+        if (!code) load_real<L>(s_rc, 1, rc.x);
         if (tr) p.trace[j * 8 + 6] = g2_timer();
         // code is cluster-uniform (same tree, same r_kk in every CTA); an
         // overflow while dividing rows is local: it is recorded and stops the
