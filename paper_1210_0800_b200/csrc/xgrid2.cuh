@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
             // back off while waiting: dozens of clusters polling the L2 flat
             // out slow down everyone's loads, the critical path first
             while ((v = *(volatile int*)(p.flags + k)) < g.cs && *(volatile int*)abortw == 0)
-                __nanosleep(200);
+                __nanosleep(64);
             __threadfence();  // acquire side (pairs with the publisher's red.release)
             s_flag = (v >= g.cs && *(volatile int*)abortw == 0) ? 1 : 0;
         }
