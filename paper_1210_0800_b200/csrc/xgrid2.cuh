@@ -483,6 +483,11 @@ cudaError_t launch_grid2_t(const GridParams& p, int max_clusters, cudaStream_t s
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
+    // dev: XQR_NO_COOP=1 drops the cooperative attribute (same grid, all CTAs
+    // still co-resident in practice) so a profiler that cannot replay
+    // cooperative cluster launches can capture the kernel
+    if (const char* e = std::getenv("XQR_NO_COOP"))
+        if (e[0] == '1') cfg.numAttrs = 1;
     // as many clusters as fit co-resident (and no more than there are columns)
     int nclusters = 0;
     cfg.gridDim = dim3(p.cs, 1, 1);
