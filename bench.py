@@ -220,6 +220,7 @@ def main():
     ap.add_argument("--no-single", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    args.e2e_steps = max(1, args.e2e_steps)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
