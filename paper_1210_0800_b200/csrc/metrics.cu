@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256) residual_kernel(int m, int n, const doubl
         for (int l = 0; l <= j; ++l)
             s = cadd(s, cmul(load_aos<L>(Q + ((int64_t)l * m + i) * L2), load_aos<L>(Rm + ((int64_t)j * n + l) * L2)));
         worst = cabs_ref<L>(csub(load_aos<L>(A + ((int64_t)j * m + i) * L2), s));
-        bad = !finite(head(worst));
+        bad = !vfinite(worst);
     }
     block_max<L>(worst, bad, part + (sys * gridDim.x + blockIdx.x) * L, flags + sys);
 }
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) orthodefect_kernel(int m, int n, int rpl,
         acc = warp_tree(acc, lane, m, rpl);
         if (i == j) acc.re = sub(acc.re, rmake<R>(1.0));
         worst = cabs_ref<L>(acc);
-        bad = !finite(head(worst));
+        bad = !vfinite(worst);
         worst = shfl_idx_r(worst, 0);
         bad = __shfl_sync(0xffffffffu, (int)bad, 0) != 0;
     }

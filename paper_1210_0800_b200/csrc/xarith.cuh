@@ -182,6 +182,13 @@ XB_DEV r4 rmake<r4>(double v) { return make4(v); }
 XB_DEV double head(const r1& a) { return a.c0; }
 XB_DEV double head(const r2& a) { return a.c0; }
 XB_DEV double head(const r4& a) { return a.c0; }
+// Overflow detection as the reference has it: double-double and quad-double
+// arithmetic is checked (double_double.hpp:35, quad_double.hpp:203, eft.hpp:78-84
+// raise overflow_error on a non-finite leading component), plain double is
+// not (real_type.hpp:19) -- complex<double> results propagate Inf/NaN.
+XB_DEV bool vfinite(const r1&) { return true; }
+XB_DEV bool vfinite(const r2& a) { return finite(a.c0); }
+XB_DEV bool vfinite(const r4& a) { return finite(a.c0); }
 
 // ---- double ---------------------------------------------------------------
 XB_DEV r1 add(const r1& a, const r1& b) { return {dadd(a.c0, b.c0)}; }
@@ -1237,7 +1244,7 @@ XB_DEV cx<R> cdiv(const cx<R>& a, const cx<R>& b, int& status) {
 
 template <class R>
 XB_DEV bool cfinite(const cx<R>& z) {
-    return finite(head(z.re)) && finite(head(z.im));
+    return vfinite(z.re) && vfinite(z.im);
 }
 
 // ---- limb load / store with a plane stride ------------------------------------

@@ -43,7 +43,7 @@ XB_DEV int arith_elem(int op, const double* pa, const double* pb, double* po) {
             case 8: o = renormalize(x); break;
             default: code = 5; o = x;
         }
-        if (L > 1 && !code && op != 8 && !finite(head(o))) code = 2;
+        if (L > 1 && !code && op != 8 && !vfinite(o)) code = 2;
         store_real<L>(po, 1, o);
     } else {
         C x, y, o;

@@ -100,7 +100,7 @@ XB_DEVICE void cta_backsub_prep(int n, const double* r, const double* y, double*
                 s.t = rdiv(d.re, d.im, dst);
                 s.d = add(mul(d.re, s.t), d.im);
             }
-            if (!dst && (!finite(head(s.t)) || !finite(head(s.d)))) dst = 2;
+            if (!dst && (!vfinite(s.t) || !vfinite(s.d))) dst = 2;
             if (!dst) s.rc = recip(s.d, dst);
         }
         s.code = dst;
@@ -139,7 +139,7 @@ XB_DEVICE bool cta_back_substitute(int n, const double* r, const double* y, doub
                 s.t = rdiv(d.re, d.im, dst);
                 s.d = add(mul(d.re, s.t), d.im);
             }
-            if (!dst && (!finite(head(s.t)) || !finite(head(s.d)))) dst = 2;
+            if (!dst && (!vfinite(s.t) || !vfinite(s.d))) dst = 2;
             if (!dst) s.rc = recip(s.d, dst);
         }
         s.code = dst;
@@ -236,7 +236,7 @@ XB_DEVICE bool pair_back_substitute(int n, const double* r, const double* y, dou
             err = true;
         } else {
             v = smith(are, aim, n - 1);
-            if (!finite(head(v)) || !finite(head(shfl_pair(v, pmask)))) {
+            if (!vfinite(v) || !vfinite(shfl_pair(v, pmask))) {
                 if (part == 0) atomicMin(key, status_key(pos_base, 0, 2));
                 err = true;
             }
@@ -262,7 +262,7 @@ XB_DEVICE bool pair_back_substitute(int n, const double* r, const double* y, dou
             rpair<R> pr = mul2(rre, y1, rim, y2);
             const R t = add(pr.x, part ? pr.y : neg(pr.y));
             R v = sub(xj, t);  // csub (complex.hpp:31-34)
-            bool bad = !finite(head(v)) || !finite(head(shfl_pair(v, pmask)));
+            bool bad = !vfinite(v) || !vfinite(shfl_pair(v, pmask));
             if (bad) {
                 if (part == 0) atomicMin(key, status_key(pos_base + (n - 1 - k), 0, 2));
                 err = true;
@@ -274,7 +274,7 @@ XB_DEVICE bool pair_back_substitute(int n, const double* r, const double* y, dou
                 } else {
                     const R o = shfl_pair(v, pmask);
                     v = smith(part ? o : v, part ? v : o, j);
-                    if (!finite(head(v)) || !finite(head(shfl_pair(v, pmask)))) {
+                    if (!vfinite(v) || !vfinite(shfl_pair(v, pmask))) {
                         if (part == 0) atomicMin(key, status_key(pos_base + (n - k), 0, 2));
                         err = true;
                     }
@@ -293,6 +293,195 @@ XB_DEVICE bool pair_back_substitute(int n, const double* r, const double* y, dou
         if (__syncthreads_or(err)) return true;
     }
     return false;
+}
+
+
+// Warp-specialised form of pair_back_substitute for one system (same
+// lane-pair split, same operations and order per unknown, mgs.hpp:117-124),
+// without a CTA barrier per step.  The sequential chain of the column sweep is
+//   x_k final -> x_{k-1} -= r_{k-1,k} x_k -> Smith division of x_{k-1},
+// and every other update x_j -= r_jk x_k (j <= k-2) can run a step or more
+// behind it.  So:
+//   * warp 0 is the FINISHER: its lane pair 0 applies the last update to
+//     x_{k-1}, divides it, keeps it in registers for the next step and
+//     publishes it (shared memory + a monotone `frontier`);
+//   * warps 1..NW-1 are UPDATERS: unknowns are dealt to them in blocks of 16
+//     (one per lane pair); for every published x_k, in order, an updater
+//     applies x_j -= r_jk x_k to its own j <= k-2 and then advances its
+//     `done` mark, which is what the finisher waits for before taking x_{k-1}.
+// Nothing on the chain waits for a CTA barrier or for another pair's
+// data-dependent (divergent) add paths; R is read ahead into registers.
+//
+// Errors (the reference raises the first in program order): a failing
+// divide of x_k or update at step k records its status key and raises
+// `stop` to k; a warp stops before any step k <= stop, so every step above
+// the first failure is completed by every warp and the minimum key is the
+// reference's.  xs (n*2L doubles), prep (n*(3L+1)) and sync (2 + NW ints)
+// are shared memory; blockDim.x is a multiple of 32, at least 64.  Returns
+// (uniformly) true on error.
+template <int L>
+XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, double* xs, double* prep,
+                                    int* sync, unsigned long long* key, long long pos_base,
+                                    unsigned long long* trace = nullptr) {
+    using R = real_t<L>;
+    constexpr unsigned kFull = 0xffffffffu;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
+    const int part = lane & 1, pl = lane >> 1, NU = NW - 1, BW = 16 * NU;
+    const unsigned pmask = 3u << (lane & 30);
+    volatile int* frontier = sync;  // lowest k whose x_k is final and in xs
+    volatile int* stop = sync + 1;  // highest step at which an error occurred
+    volatile int* done = sync + 2;  // done[w]: updater w applied every x_k, k >= done[w]
+    cta_backsub_prep<L>(n, r, y, xs, prep);
+    if (tid == 0) {
+        sync[0] = n;
+        sync[1] = -1;
+    }
+    if (tid < NW) sync[2 + tid] = n;
+    __syncthreads();
+    bool err = false;
+    auto fail = [&](int step, int code) {
+        if (part == 0) {
+            atomicMin(key, status_key(pos_base + (n - 1 - step), 0, code));
+            atomicMax((int*)stop, step);
+        }
+        err = true;
+    };
+    auto xs_part = [&](int j, int pp) { return xs + (size_t)j * 2 * L + pp * L; };
+    auto rpart = [&](int j, int k, int pp) { return r + ((size_t)k * n + j) * 2 * L + pp * L; };
+    // own half of Smith(x / d_j) (complex.hpp:50-57), R-only parts from prep
+    auto smith = [&](const R& are, const R& aim, int j, int& code) -> R {
+        const smith_prep<L> sp = prep_load<L>(prep + (size_t)j * (3 * L + 1));
+        code = sp.code;
+        R num;
+        if (sp.br) {
+            const R prod = mul(part ? are : aim, sp.t);
+            num = add(part ? aim : are, part ? neg(prod) : prod);
+        } else {
+            const R prod = mul(part ? aim : are, sp.t);
+            num = add(prod, part ? neg(are) : aim);
+        }
+        return divide(num, sp.d, sp.rc);
+    };
+    // own half of x_j - r_jk x_k (cmul complex.hpp:41-44, csub :31-34), given
+    // this lane's (y1, y2) = (x_k.re, x_k.im) or (x_k.im, x_k.re)
+    auto update = [&](const R& xj, const R& rre, const R& rim, const R& y1, const R& y2) -> R {
+        rpair<R> pr = mul2(rre, y1, rim, y2);
+        return sub(xj, add(pr.x, part ? pr.y : neg(pr.y)));
+    };
+
+    if (warp == 0) {
+        // ---------------- finisher ----------------
+        if (lane < 2) {
+            int code = 0;
+            R are, aim;
+            load_real<L>(xs_part(n - 1, 0), 1, are);
+            load_real<L>(xs_part(n - 1, 1), 1, aim);
+            R v = smith(are, aim, n - 1, code);  // x_{n-1} = y_{n-1} / r_{n-1,n-1}
+            if (code) {
+                fail(n - 1, code);
+            } else if (!vfinite(v) || !vfinite(shfl_pair(v, pmask))) {
+                fail(n - 1, 2);
+            }
+            R rre, rim;  // r_{k-1,k} for the next step, read ahead
+            if (n >= 2) {
+                load_real<L>(rpart(n - 2, n - 1, 0), 1, rre);
+                load_real<L>(rpart(n - 2, n - 1, 1), 1, rim);
+            }
+            store_real<L>(xs_part(n - 1, part), 1, v);
+            __syncwarp(3u);
+            if (lane == 0) {
+                __threadfence_block();
+                *frontier = n - 1;
+            }
+            for (int k = n - 1; k >= 1 && !err; --k) {
+                // dev instrumentation (XQR_GRID_TRACE): SM cycles per phase
+                unsigned long long c0 = trace ? clock64() : 0;
+                // x_{k-1} has every update but x_k's once its updater is past k+1
+                const int w = 1 + ((k - 1) >> 4) % NU;
+                while (done[w] > k + 1 && *stop < k) __nanosleep(20);
+                __threadfence_block();
+                unsigned long long c1 = trace ? clock64() : 0, c2 = 0;
+                if (*stop >= k) break;
+                // (y1, y2) = (own half, other half) of x_k
+                const R y1 = v, y2 = shfl_pair(v, 3u);
+                R xj;
+                load_real<L>(xs_part(k - 1, part), 1, xj);
+                const R cr = rre, ci = rim;
+                if (k >= 2) {  // read ahead r_{k-2,k-1}
+                    load_real<L>(rpart(k - 2, k - 1, 0), 1, rre);
+                    load_real<L>(rpart(k - 2, k - 1, 1), 1, rim);
+                }
+                v = update(xj, cr, ci, y1, y2);
+                if (!vfinite(v) || !vfinite(shfl_pair(v, 3u))) {
+                    fail(k, 2);
+                } else {
+                    if (trace) c2 = clock64();
+                    const R ov = shfl_pair(v, 3u);
+                    v = smith(part ? ov : v, part ? v : ov, k - 1, code);
+                    if (code) {
+                        fail(k - 1, code);
+                    } else if (!vfinite(v) || !vfinite(shfl_pair(v, 3u))) {
+                        fail(k - 1, 2);
+                    }
+                }
+                unsigned long long c3 = trace ? clock64() : 0;
+                store_real<L>(xs_part(k - 1, part), 1, v);
+                __syncwarp(3u);
+                if (lane == 0) {
+                    __threadfence_block();
+                    *frontier = k - 1;
+                }
+                if (trace && lane == 0) {
+                    trace[8 * k + 0] = c0;
+                    trace[8 * k + 1] = c1;
+                    trace[8 * k + 2] = c2;
+                    trace[8 * k + 3] = c3;
+                    trace[8 * k + 4] = clock64();
+                }
+            }
+        }
+    } else {
+        // ---------------- updaters ----------------
+        const int base = 16 * (warp - 1) + pl;  // this pair's lowest unknown
+        int k = n - 1;
+        for (; k >= 2; --k) {
+            if (16 * (warp - 1) > k - 2) break;  // every own unknown is past its updates
+            if (lane == 0)
+                while (*frontier > k && *stop < k) __nanosleep(32);
+            __syncwarp();
+            __threadfence_block();
+            if (__any_sync(kFull, *stop >= k)) break;
+            R xkre, xkim;
+            load_real<L>(xs_part(k, 0), 1, xkre);
+            load_real<L>(xs_part(k, 1), 1, xkim);
+            const R y1 = part ? xkim : xkre, y2 = part ? xkre : xkim;
+            // highest own j <= k-2 first: the finisher needs x_{k-2} next
+            for (int j = base <= k - 2 ? base + ((k - 2 - base) / BW) * BW : -1; j >= 0; j -= BW) {
+#ifdef XB_BS_EXPERIMENT
+                continue;
+#endif
+                R rre, rim, xj;
+                load_real<L>(rpart(j, k, 0), 1, rre);
+                load_real<L>(rpart(j, k, 1), 1, rim);
+                load_real<L>(xs_part(j, part), 1, xj);
+                const R v = update(xj, rre, rim, y1, y2);
+                if (!vfinite(v) || !vfinite(shfl_pair(v, pmask))) fail(k, 2);
+                store_real<L>(xs_part(j, part), 1, v);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                done[warp] = k;
+            }
+            // R is known from the start: pull next step's r_{j,k-1} into L1
+            for (int j = base <= k - 3 ? base + ((k - 3 - base) / BW) * BW : -1; j >= 0; j -= BW)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(rpart(j, k - 1, part)));
+        }
+        __syncwarp();
+        if (lane == 0 && k < 2) done[warp] = -1;  // nothing left: never hold the finisher
+        if (lane == 0 && k >= 2 && 16 * (warp - 1) > k - 2) done[warp] = -1;
+    }
+    return __syncthreads_or(err);
 }
 
 }  // namespace xb

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
     for (int j = c; j < ncol; j += G) {
         R s = col_sq(colp(j));
         R nrm = rsqrt_ref(s);
-        if (!finite(head(s)) || !finite(head(nrm))) {
+        if (!vfinite(s) || !vfinite(nrm)) {
             if (tid == 0) record(0, 0, XQR_OVERFLOW);
         }
         if (tid == 0) store_real<L>(p.norms + (int64_t)j * L, 1, nrm);
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
         R s = col_sq(col);
         R rkk = rsqrt_ref(s);
         int code = 0;
-        if (!finite(head(s)) || !finite(head(rkk))) code = XQR_OVERFLOW;
+        if (!vfinite(s) || !vfinite(rkk)) code = XQR_OVERFLOW;
         else if (le(rkk, thr)) code = XQR_BREAKDOWN;
         recip_t<R> rc;
         if (!code) {
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
         R s = col_sq(colp(n));
         R z = rsqrt_ref(s);
         if (tid == 0) {
-            if (!finite(head(s)) || !finite(head(z))) record(1 + (long long)n * (ncol + 1), 0, XQR_OVERFLOW);
+            if (!vfinite(s) || !vfinite(z)) record(1 + (long long)n * (ncol + 1), 0, XQR_OVERFLOW);
             store_real<L>(p.z, 1, z);
         }
     }

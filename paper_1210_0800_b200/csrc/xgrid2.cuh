@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
         R s = col_norm2(g.col(j));
         R nrm = rsqrt_ref(s);
         if (g.crank == 0 && g.tid == 0) {
-            if (!finite(head(s)) || !finite(head(nrm))) record(0, 0, XQR_OVERFLOW);
+            if (!vfinite(s) || !vfinite(nrm)) record(0, 0, XQR_OVERFLOW);
             store_real<L>(p.norms + (int64_t)j * L, 1, nrm);
         }
     }
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
             R rkk0 = rsqrt_ref(s);
             if (tr) p.trace[j * 8 + 5] = g2_timer();
             int code0 = 0;
-            if (!finite(head(s)) || !finite(head(rkk0)))
+            if (!vfinite(s) || !vfinite(rkk0))
                 code0 = XQR_OVERFLOW;
             else if (le(rkk0, thr))
                 code0 = XQR_BREAKDOWN;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
         if (!code) {
             for (int t = 0; t < g.cnt; ++t) {
                 R v = divide(g.ld_part(c, g.row0 + t), rkk, rc);
-                if (!finite(head(v))) ok = false;
+                if (!vfinite(v)) ok = false;
                 g.st_part(c, g.row0 + t, v);
             }
         }
@@ -355,14 +355,14 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
             R ro = shfl_xor_r(rh, 1);
             r.re = g.part ? ro : rh;
             r.im = g.part ? rh : ro;
-            bool ok = finite(head(r.re)) && finite(head(r.im));
+            bool ok = vfinite(r.re) && vfinite(r.im);
             // a_i -= r * q_i (mgs.hpp:59): t = cmul(r, q_i), a - t
             for (int t = 0; t < g.cnt; ++t) {
                 const R y1 = g.part ? q[t].im : q[t].re, y2 = g.part ? q[t].re : q[t].im;
                 rpair<R> pr = mul2(r.re, y1, r.im, y2);
                 R tt = add(pr.x, g.part ? pr.y : neg(pr.y));
                 R v = sub(g.ld_part(c, g.row0 + t), tt);
-                if (!finite(head(v))) ok = false;
+                if (!vfinite(v)) ok = false;
                 g.st_part(c, g.row0 + t, v);
             }
             ok = __syncthreads_and(ok);
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
         R s = col_norm2(g.col(n));
         R z = rsqrt_ref(s);
         if (g.tid == 0 && g.crank == 0) {
-            if (!finite(head(s)) || !finite(head(z))) record(1 + (long long)n * (ncol + 1), 0, XQR_OVERFLOW);
+            if (!vfinite(s) || !vfinite(z)) record(1 + (long long)n * (ncol + 1), 0, XQR_OVERFLOW);
             store_real<L>(p.z, 1, z);
         }
     }
@@ -424,22 +424,29 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
 }
 
 // Back substitution of the single-system least-squares solve (mgs.hpp:157 ->
-// :110-126): one CTA of kG2BsThreads threads = one lane pair per unknown for
-// n <= 256, so the lane that divides x_{k-1} has no other update in its step.
+// :110-126): one CTA of kG2BsThreads threads, one lane pair per unknown for
+// n <= 256 warp-specialised (flow_back_substitute): a finisher warp runs the
+// chain, updater warps trail it; no CTA barrier per step.
 constexpr int kG2BsThreads = 512;
+template <int L>
+constexpr size_t g2_backsub_smem(int n) {
+    return sizeof(double) * (size_t)n * (2 * L + 3 * L + 1);
+}
 template <int L>
 __global__ void __launch_bounds__(kG2BsThreads, 1) grid2_backsub_kernel(GridParams p) {
     constexpr int L2 = 2 * L;
     extern __shared__ double xs[];
     __shared__ unsigned long long s_key;
+    __shared__ int s_sync[2 + 32];
     const int n = p.n, ncol = n + 1;
     if (threadIdx.x == 0) s_key = *p.key;
     __syncthreads();
     if (s_key != kNoError) return;  // status already written by the factorisation
     if (p.trace && threadIdx.x == 0) p.trace[n * 8 + 5] = g2_timer();
-    double* ydst = p.rws + (int64_t)n * n * L2;
-    double* prep = ydst + (int64_t)n * L2;
-    bool bad = pair_back_substitute<L>(n, p.rws, ydst, xs, prep, &s_key, 2 + (long long)n * (ncol + 1));
+    const double* ydst = p.rws + (int64_t)n * n * L2;
+    double* prep = xs + (size_t)n * L2;
+    bool bad = flow_back_substitute<L>(n, p.rws, ydst, xs, prep, s_sync, &s_key,
+                                       2 + (long long)n * (ncol + 1), p.trace);
     if (!bad)
         for (int e = threadIdx.x; e < n * L2; e += blockDim.x) p.x[e] = xs[e];
     __syncthreads();
@@ -502,29 +509,30 @@ cudaError_t launch_grid2_t(const GridParams& p, int max_clusters, cudaStream_t s
     if (nclusters > ncol) nclusters = ncol;
     if (nclusters < 1) return cudaErrorInvalidConfiguration;
     cfg.gridDim = dim3(nclusters * p.cs, 1, 1);
-    e = cudaLaunchKernelEx(&cfg, kern, p);
-    if (e != cudaSuccess || !LSQ) return e;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+// The back substitution of a least-squares solve, launched after the grid
+// kernel on the same stream.
+template <int L>
+cudaError_t launch_grid2_backsub(const GridParams& p, cudaStream_t s) {
     auto bs = grid2_backsub_kernel<L>;
-    const size_t bsmem = sizeof(double) * (size_t)p.n * 2 * L;
+    const size_t bsmem = g2_backsub_smem<L>(p.n);
     if (bsmem > 48 * 1024) {
-        e = cudaFuncSetAttribute(bs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+        cudaError_t e = cudaFuncSetAttribute(bs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
         if (e != cudaSuccess) return e;
     }
     bs<<<1, kG2BsThreads, bsmem, s>>>(p);
     return cudaGetLastError();
 }
 
-template <int L>
-cudaError_t launch_grid2(const GridParams& p, bool lsq, int max_clusters, cudaStream_t s) {
-    switch (p.rpt) {
-        case 1: return lsq ? launch_grid2_t<L, 1, true>(p, max_clusters, s)
-                           : launch_grid2_t<L, 1, false>(p, max_clusters, s);
-        case 2: return lsq ? launch_grid2_t<L, 2, true>(p, max_clusters, s)
-                           : launch_grid2_t<L, 2, false>(p, max_clusters, s);
-        case 4: return lsq ? launch_grid2_t<L, 4, true>(p, max_clusters, s)
-                           : launch_grid2_t<L, 4, false>(p, max_clusters, s);
-        default: return cudaErrorInvalidValue;
-    }
+// RPP = 1 (m <= 256) and RPP = 2, 4 (m <= 1024) are instantiated in
+// separate translation units (mgs_grid_L4.cu, mgs_grid_L4w.cu) so each can be
+// compiled with the call-form mix it is fastest with (Makefile).
+template <int L, int RPP>
+cudaError_t launch_grid2_rpp(const GridParams& p, bool lsq, int max_clusters, cudaStream_t s) {
+    return lsq ? launch_grid2_t<L, RPP, true>(p, max_clusters, s)
+               : launch_grid2_t<L, RPP, false>(p, max_clusters, s);
 }
 
 }  // namespace xb

@@ -80,7 +80,7 @@ struct mgs_warp {
                                 R& rkk) {
         R s = col_sq(f, col, lane, m);
         rkk = rsqrt_ref(s);
-        if (!finite(head(s)) || !finite(head(rkk))) return 2;
+        if (!vfinite(s) || !vfinite(rkk)) return 2;
         if (le(rkk, thr)) return 1;
         int st = 0;
         recip_t<R> rc = recip(rkk, st);
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) mgs_cta_kernel(SolveParams p, i
         for (int j = warp; j < ncol; j += NW) {
             R s = W::col_sq(f, ws + (int64_t)j * f.COL, lane, m);
             R nrm = rsqrt_ref(s);
-            if (!finite(head(s)) || !finite(head(nrm))) err = true;
+            if (!vfinite(s) || !vfinite(nrm)) err = true;
             if (lt(best, nrm)) best = nrm;
         }
         if (lane == 0) {
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) mgs_cta_kernel(SolveParams p, i
             if (warp == 0) {
                 R s = W::col_sq(f, ws + (int64_t)n * f.COL, lane, m);
                 R z = rsqrt_ref(s);
-                if (!finite(head(s)) || !finite(head(z))) {
+                if (!vfinite(s) || !vfinite(z)) {
                     if (lane == 0)
                         atomicMin(&s_key,
                                   status_key(1 + (long long)n * (ncol + 1), 0, XQR_OVERFLOW));

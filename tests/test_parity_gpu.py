@@ -171,6 +171,52 @@ def test_overflow_reported(port, L):
         xqr.mgs_qr(a)
 
 
+def assert_same_nan(got, want, what=""):
+    """Bitwise where the oracle is a number; NaN where it is NaN (the GPU's
+    canonical NaN and x86's default NaN differ in sign and payload bits)."""
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(got), nan), f"{what}: NaN positions differ"
+    assert_same(np.where(nan, 0.0, got), np.where(nan, 0.0, want), what)
+
+
+def test_cd_overflow_propagates(port):
+    """complex<double> arithmetic is unchecked in the reference
+    (real_type.hpp:19): Inf/NaN propagate and no overflow_error is raised,
+    unlike dd/qd (test_overflow_reported).  A column norm that overflows
+    to Inf still trips the breakdown test (mgs.hpp:84-92), as in the
+    reference; a back substitution that overflows just returns Inf/NaN."""
+    a = np.zeros((2, 2, 2, 1))
+    a[0, 0, 0, 0] = 1e300
+    a[0, 1, 0, 0] = 1e300
+    a[1, 0, 0, 0] = 1.0
+    a[1, 1, 1, 0] = 1.0
+    q, r, st = port.mgs_qr(a)
+    assert st[0] == 1
+    with pytest.raises(xqr.breakdown_error) as e:
+        xqr.mgs_qr(a)
+    assert e.value.column == st[1]
+    a = np.zeros((2, 2, 2, 1))
+    a[0, :, 0, 0] = (1e150, 1e150)  # |a_0|^2 finite, r_01 * q_0 overflows
+    a[1, :, 0, 0] = (1e300, -1e300)
+    a[1, 1, 1, 0] = 1.0
+    q, r, st = port.mgs_qr(a)
+    if st[0] == 1:
+        with pytest.raises(xqr.breakdown_error):
+            xqr.mgs_qr(a)
+    else:
+        assert st[0] == 0
+        gq, gr = xqr.mgs_qr(a)
+        assert_same_nan(gq, q, "Q")
+        assert_same_nan(gr, r, "R")
+    rng = np.random.default_rng(5)
+    rr, y = _upper(rng, 40, 1)
+    rr[30, :30, :, 0] = 1e300
+    y[30, :, 0] = 1e300
+    x, st = port.back_substitute(rr, y)
+    assert st == (0, 0)
+    assert_same_nan(xqr.back_substitute(rr, y), x, "back substitution")
+
+
 @pytest.mark.parametrize("L", [2, 4])
 @pytest.mark.parametrize("m,n", [(70, 20), (24, 12)])
 def test_single_system_grid_error_paths(port, L, m, n):
@@ -232,6 +278,41 @@ def test_back_substitute_api(port, L):
         xqr.back_substitute(np.zeros((2, 3, 2, L)), y)
     with pytest.raises(xqr.dimension_error):
         xqr.back_substitute(np.eye(3)[:, :, None, None] * np.ones((1, 1, 2, L)), y)
+
+
+def _upper(rng, n, L):
+    r = np.zeros((n, n, 2, L))
+    for j in range(n):
+        r[j, : j + 1, :, 0] = rng.uniform(-1, 1, (j + 1, 2))
+        r[j, j, :, 0] += (1.5, 0.25)
+    y = np.zeros((n, 2, L))
+    y[..., 0] = rng.uniform(-1, 1, (n, 2))
+    return r, y
+
+
+@pytest.mark.parametrize("L", [1, 2, 4])
+def test_back_substitute_flow(port, L):
+    """Single-system back substitution runs the warp-pipelined sweep
+    (flow_back_substitute): sizes with one and several unknowns per lane
+    pair, and the reference's first error when several are planted --
+    an overflowing update above a zero diagonal (the overflow comes first in
+    program order, mgs.hpp:117-124) and the other way round."""
+    rng = np.random.default_rng(100 + L)
+    for n in (16, 17, 255, 256, 257, 300, 513):
+        r, y = _upper(rng, n, L)
+        x, st = port.back_substitute(r, y)
+        assert st == (0, 0)
+        assert_same(xqr.back_substitute(r, y), x, f"n={n}")
+    n = 300
+    for k_over, k_zero in ((250, 100), (40, 200), (299, 17), (5, 6)):
+        r, y = _upper(rng, n, L)
+        r[k_over, : k_over, :, 0] = 1e300  # x_j -= r_jk x_k overflows at step k_over
+        y[k_over, :, 0] = 1e300
+        r[k_zero, k_zero] = 0.0  # zero diagonal -> domain_error at step k_zero
+        _, st = port.back_substitute(r, y)
+        assert st[0] in (2, 3)
+        with pytest.raises({2: xqr.overflow_error, 3: xqr.domain_error}[st[0]]):
+            xqr.back_substitute(r, y)
 
 
 @pytest.mark.parametrize("L", [2, 4])

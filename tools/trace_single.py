@@ -1,0 +1,49 @@
+"""Phase timing of one single-system grid solve (dev tool): runs lsq_solve on
+the reference generator's system with XQR_GRID_TRACE set and prints the
+factorisation and back-substitution spans from the device timestamps.
+
+    python tools/trace_single.py [--limbs 4] [--m 256] [--n 256] [--reps 3]
+"""
+import argparse
+import os
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--limbs", type=int, default=4)
+    ap.add_argument("--m", type=int, default=256)
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--phases", action="store_true", help="finisher phase cycles (back substitution)")
+    args = ap.parse_args()
+    path = os.path.join(tempfile.mkdtemp(), "trace.txt")
+    os.environ["XQR_GRID_TRACE"] = path
+    import paper_1210_0800_b200 as xqr
+
+    a, b = xqr.gen_systems(args.limbs, 1, args.m, args.n, 1.0, 1, -1)
+    for rep in range(args.reps):
+        xqr.lsq_solve(a[0], b[0])
+        t = np.loadtxt(path, dtype=np.uint64)
+        last = t[-1]
+        start, grid_end, bs_start, bs_end = int(last[8]), int(last[5]), int(last[6]), int(last[7])
+        fact = (grid_end - start) / 1e3 if start else float("nan")
+        if args.phases:
+            c = t[1:-1, 1:6].astype(np.int64)  # back-substitution steps k = 1 .. n-1
+            c = c[c[:, 0] != 0]
+            ph = np.diff(c, axis=1).mean(axis=0)
+            loop = (c[:-1, 0] - c[1:, 4]).mean() if len(c) > 1 else 0
+            print(f"  finisher cycles/step: wait {ph[0]:.0f}, update {ph[1]:.0f}, smith {ph[2]:.0f}, "
+                  f"publish {ph[3]:.0f}, loop {loop:.0f}")
+        print(f"rep {rep}: factorisation {fact:.1f} us, gap {(bs_start - grid_end) / 1e3:.1f} us, "
+              f"back substitution {(bs_end - bs_start) / 1e3:.1f} us", flush=True)
+
+
+if __name__ == "__main__":
+    main()
