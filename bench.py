@@ -389,7 +389,7 @@ def main():
             "roofline": {"bound": "fp64", "achieved": achieved_instr / 1e12,
                          "peak": FP64_PEAK_INSTR / 1e12, "unit": "T FP64 instr/s",
                          "frac": achieved_instr / FP64_PEAK_INSTR, "traffic": traffic,
-                         "kernel": "mgs_cta_kernel<4,3,4,true>",
+                         "kernel": "mgs_cta_kernel<L=4,LV=3,NW=8,LSQ,MINB=2> (8 warps x 2 CTAs per SM)",
                          "fp64_tflops": flops * per_rank / kernel_s / 1e12,
                          "fp64_tflops_peak": FP64_PEAK_FLOPS / 1e12,
                          "peak_source": "measured (profiles/r01_fp64_probe.log): MEASURED_PEAKS.json "
