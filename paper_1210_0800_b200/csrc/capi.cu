@@ -176,7 +176,7 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     const size_t o_flg = plan.add(sizeof(int) * ((size_t)n + 4));
     const size_t o_key = plan.add(sizeof(unsigned long long));
     const char* trace_path = std::getenv("XQR_GRID_TRACE");  // dev instrumentation
-    const size_t o_trc = plan.add(trace_path ? sizeof(unsigned long long) * 8 * (size_t)(n + 1) : 0);
+    const size_t o_trc = plan.add(trace_path ? sizeof(unsigned long long) * 16 * (size_t)(n + 1) : 0);
     cudaError_t e = ensure_arena(ctx, scratch_off + plan.total + 256);
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
     p.ws = reinterpret_cast<double*>(at(ctx, scratch_off + o_ws));
@@ -188,7 +188,7 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     p.trace = trace_path ? reinterpret_cast<unsigned long long*>(at(ctx, scratch_off + o_trc)) : nullptr;
     cudaMemsetAsync(p.flags, 0, sizeof(int) * ((size_t)n + 4), ctx->stream);
     cudaMemsetAsync(p.key, 0xFF, sizeof(unsigned long long), ctx->stream);
-    if (p.trace) cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * 8 * (size_t)(n + 1), ctx->stream);
+    if (p.trace) cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * 16 * (size_t)(n + 1), ctx->stream);
     int per_sm = limbs == 4 ? xb::kGrid2PerSM : 1;
     if (const char* e = std::getenv("XQR_GRID_PER_SM")) per_sm = std::max(1, std::atoi(e));  // dev
     const int max_clusters = per_sm * ctx->num_sms / p.cs;
@@ -203,14 +203,19 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     ctx->launches += 1;
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "grid kernel launch");
     if (p.trace) {
-        std::vector<unsigned long long> h(8 * (size_t)(n + 1));
+        // per row j: 8 factorisation stamps (globaltimer), then 8 back-substitution
+        // stamps (SM cycles) -- dev instrumentation, XQR_GRID_TRACE
+        std::vector<unsigned long long> h(16 * (size_t)(n + 1));
         cudaMemcpyAsync(h.data(), p.trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
                         ctx->stream);
         cudaStreamSynchronize(ctx->stream);
         if (FILE* fp = std::fopen(trace_path, "w")) {
-            for (int j = 0; j <= n; ++j)
-                std::fprintf(fp, "%d %llu %llu %llu %llu %llu %llu %llu %llu\n", j, h[8 * j], h[8 * j + 1],
-                             h[8 * j + 2], h[8 * j + 3], h[8 * j + 4], h[8 * j + 5], h[8 * j + 6], h[8 * j + 7]);
+            for (int j = 0; j <= n; ++j) {
+                std::fprintf(fp, "%d", j);
+                for (int c = 0; c < 8; ++c) std::fprintf(fp, " %llu", h[8 * j + c]);
+                for (int c = 0; c < 8; ++c) std::fprintf(fp, " %llu", h[8 * (size_t)(n + 1) + 8 * j + c]);
+                std::fprintf(fp, "\n");
+            }
             std::fclose(fp);
         }
     }

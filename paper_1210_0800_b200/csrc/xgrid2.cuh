@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(kG2BsThreads, 1) grid2_backsub_kernel(GridPara
     const double* ydst = p.rws + (int64_t)n * n * L2;
     double* prep = xs + (size_t)n * L2;
     bool bad = flow_back_substitute<L>(n, p.rws, ydst, xs, prep, s_sync, &s_key,
-                                       2 + (long long)n * (ncol + 1), p.trace);
+                                       2 + (long long)n * (ncol + 1), p.trace ? p.trace + 8 * (n + 1) : nullptr);
     if (!bad)
         for (int e = threadIdx.x; e < n * L2; e += blockDim.x) p.x[e] = xs[e];
     __syncthreads();

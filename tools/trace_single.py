@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--phases", action="store_true", help="finisher phase cycles (back substitution)")
+    ap.add_argument("--pivots", action="store_true", help="per-pivot phases of the factorisation")
     args = ap.parse_args()
     path = os.path.join(tempfile.mkdtemp(), "trace.txt")
     os.environ["XQR_GRID_TRACE"] = path
@@ -34,8 +35,26 @@ def main():
         last = t[-1]
         start, grid_end, bs_start, bs_end = int(last[8]), int(last[5]), int(last[6]), int(last[7])
         fact = (grid_end - start) / 1e3 if start else float("nan")
+        if args.pivots:
+            # per pivot j (row j of the trace, globaltimer ns): 0 q_{j-1} in hand,
+            # 1 column j updated, 4 norm tree, 5 sqrt, 6 reciprocal, 7 divided,
+            # 2 published; 3 last cluster done with round j-1
+            T = t[:, 1:9].astype(np.int64)
+            n = args.n
+            rows = []
+            for j in range(2, n - 1):
+                cur, prv = T[j], T[j - 1]
+                if min(cur[0], cur[1], cur[2], cur[4], cur[5], cur[6], cur[7], prv[2]) == 0:
+                    continue
+                rows.append([cur[0] - prv[2], cur[1] - cur[0], cur[4] - cur[1], cur[5] - cur[4],
+                             cur[6] - cur[5], cur[7] - cur[6], cur[2] - cur[7], cur[2] - prv[2]])
+            rows = np.array(rows, dtype=np.float64) / 1e3
+            names = ["handoff", "update", "normtree", "sqrt", "recip", "divide", "publish", "pivot"]
+            for lo, hi in ((0, len(rows) // 3), (len(rows) // 3, 2 * len(rows) // 3), (2 * len(rows) // 3, len(rows))):
+                avg = rows[lo:hi].mean(axis=0)
+                print(f"  pivots {lo + 2}-{hi + 1}: " + ", ".join(f"{k} {v:.1f}" for k, v in zip(names, avg)) + " us")
         if args.phases:
-            c = t[1:-1, 1:6].astype(np.int64)  # back-substitution steps k = 1 .. n-1
+            c = t[1:-1, 9:14].astype(np.int64)  # back-substitution steps k = 1 .. n-1 (SM cycles)
             c = c[c[:, 0] != 0]
             ph = np.diff(c, axis=1).mean(axis=0)
             loop = (c[:-1, 0] - c[1:, 4]).mean() if len(c) > 1 else 0
