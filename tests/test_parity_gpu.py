@@ -448,3 +448,22 @@ def test_golden_bench_configs(port, name):
     x, z = xqr.lsq_solve(a, b)
     assert_same(x, g["x"], f"{name} x")
     assert_same(z, g["z"], f"{name} z")
+
+
+# ---- single-system grid kernels at their shape boundaries -----------------------------
+# xgrid2 (qd, m >= 16): cluster size 1/2/4 and 1/2/4 rows per lane pair switch
+# at m = 64, 128, 256, 512; xgrid1 (dd, m >= 64): rows per thread switch at
+# 256 and 512.  Few columns keep the oracle fast; every result bitwise.
+@pytest.mark.parametrize("L,m", [(4, m) for m in (16, 17, 63, 64, 65, 127, 129, 255, 257, 511, 513, 1000,
+                                                   1024)] + [(2, m) for m in (64, 65, 255, 257, 511, 513, 1024)])
+def test_grid_shape_boundaries(port, L, m):
+    for n in (4, 9):
+        a, b = port.gen_system(L, m, n, 1.0, 7000 + m + n)
+        q, r, _ = port.mgs_qr(a)
+        gq, gr = xqr.mgs_qr(a)
+        assert_same(gq, q, f"Q m={m} n={n}")
+        assert_same(gr, r, f"R m={m} n={n}")
+        x, z, _ = port.lsq_solve(a, b)
+        gx, gz = xqr.lsq_solve(a, b)
+        assert_same(gx, x, f"x m={m} n={n}")
+        assert_same(gz, z, f"z m={m} n={n}")
