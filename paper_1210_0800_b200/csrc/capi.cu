@@ -155,7 +155,8 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
         p.cs = 1;
         p.rpt = xb::grid1_rows_per_thread(m);
     } else {
-        xb::grid_shape(m, p.cs, p.rpt);
+        xb::grid_shape(m, p.cs, p.rpt, p.pair_bulk);
+        if (const char* e = std::getenv("XQR_GRID_PAIR")) p.pair_bulk = std::atoi(e);  // dev
         if (const char* e = std::getenv("XQR_GRID_CS")) {  // dev override of the cluster size
             p.cs = std::max(1, std::min(8, std::atoi(e)));
             p.rpt = 1;

@@ -142,6 +142,62 @@ XB_DEVICE real_t<L> g2_tree(const g2<L, RPP>& g, real_t<L> acc, double* slot_loc
     return shfl_idx_r(v, g.lane & 1);  // lane 0 holds re (or the real total), lane 1 im
 }
 
+// Two independent qd adds in lockstep as ONE call (add2_r4: both fast paths
+// interleave): the bulk updates of two trailing columns share every level of
+// their trees, at about the latency of one.
+XB_CALL_IF rpair<r4> addc2(const r4 a1, const r4 b1, const r4 a2, const r4 b2) {
+    return add2_r4(a1, b1, a2, b2);
+}
+XB_DEVICE rpair<r4> vadd(const rpair<r4>& a, const rpair<r4>& b) { return addc2(a.x, b.x, a.y, b.y); }
+
+// g2_tree for two columns at once (same pairing, same operands per column);
+// slots: one per column, same double buffering.
+template <int L, int RPP>
+XB_DEVICE rpair<real_t<L>> g2_tree2(const g2<L, RPP>& g, rpair<real_t<L>> acc, double* slot_a,
+                                    double* slot_b, int buf) {
+    namespace cg = cooperative_groups;
+    using R = real_t<L>;
+    const int pi = g.lane >> 1;
+#pragma unroll 1
+    for (int s = 1; s < 16; s <<= 1) {
+        const R o1 = shfl_down_r(acc.x, 2 * s), o2 = shfl_down_r(acc.y, 2 * s);
+        if ((pi & (2 * s - 1)) == 0 && (g.gpair + s) * RPP < g.m) acc = addc2(acc.x, o1, acc.y, o2);
+    }
+    const int off = ((buf * kG2Warps + g.warp) * 2 + g.part) * L;
+    if (pi == 0) {
+        store_real<L>(slot_a + off, 1, acc.x);
+        store_real<L>(slot_b + off, 1, acc.y);
+    }
+    cg::this_cluster().sync();
+    const int np = kG2Warps * g.cs;
+    const int npp = np > 16 ? np / 16 : 1;
+    const int rows_pp = 16 * RPP;
+    rpair<R> v = acc;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        if (u >= npp) break;
+        const int k = pi * npp + u;
+        if (k < np && k * rows_pp < g.m) {
+            const int roff = ((buf * kG2Warps + (k % kG2Warps)) * 2 + g.part) * L;
+            R wa, wb;
+            load_real<L>(cg::this_cluster().map_shared_rank(slot_a, k / kG2Warps) + roff, 1, wa);
+            load_real<L>(cg::this_cluster().map_shared_rank(slot_b, k / kG2Warps) + roff, 1, wb);
+            if (u == 0) {
+                v.x = wa;
+                v.y = wb;
+            } else {
+                v = addc2(v.x, wa, v.y, wb);
+            }
+        }
+    }
+#pragma unroll 1
+    for (int s = 1; s < 16; s <<= 1) {
+        const R o1 = shfl_down_r(v.x, 2 * s), o2 = shfl_down_r(v.y, 2 * s);
+        if ((pi & (2 * s - 1)) == 0 && (pi + s) * npp * rows_pp < g.m) v = addc2(v.x, o1, v.y, o2);
+    }
+    return {shfl_idx_r(v.x, g.lane & 1), shfl_idx_r(v.y, g.lane & 1)};
+}
+
 template <int L, int RPP, bool LSQ>
 __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) {
     namespace cg = cooperative_groups;
@@ -150,6 +206,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
     constexpr int L2 = 2 * L;
 
     __shared__ double slot[2 * kG2Warps * 2 * L];
+    __shared__ double slot2[2 * kG2Warps * 2 * L];  // second column of a paired update
     __shared__ int s_flag;
 
     g2<L, RPP> g;
@@ -339,6 +396,53 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
         if (p.trace && g.tid == 0 && g.crank == 0 && j0 == k + 1) p.trace[(k + 1) * 8 + 0] = g2_timer();
         const long long pos_k = 1 + (long long)k * (ncol + 1);
         for (int j = j0; j < ncol; j += G) {
+            if (p.pair_bulk && j != k + 1 && j + G < ncol) {
+                // two trailing columns off the critical path, in lockstep:
+                // per column exactly the single-column operations below
+                const int j2 = j + G;
+                double* c1 = g.col(j);
+                double* c2 = g.col(j2);
+                rpair<R> acc = lane_tree<(RPP >= 4 ? 3 : 2), rpair<R>>(g.cnt, [&](int t) {
+                    const C a1 = g.ld_row(c1, g.row0 + t), a2 = g.ld_row(c2, g.row0 + t);
+                    const rpair<R> p1 = mul2(q[t].re, g.part ? a1.im : a1.re, neg(q[t].im), g.part ? a1.re : a1.im);
+                    const rpair<R> p2 = mul2(q[t].re, g.part ? a2.im : a2.re, neg(q[t].im), g.part ? a2.re : a2.im);
+                    return addc2(p1.x, g.part ? p1.y : neg(p1.y), p2.x, g.part ? p2.y : neg(p2.y));
+                });
+                const rpair<R> rh = g2_tree2<L, RPP>(g, acc, slot, slot2, buf);
+                buf ^= 1;
+                const R ro1 = shfl_xor_r(rh.x, 1), ro2 = shfl_xor_r(rh.y, 1);
+                C r1, r2;
+                r1.re = g.part ? ro1 : rh.x;
+                r1.im = g.part ? rh.x : ro1;
+                r2.re = g.part ? ro2 : rh.y;
+                r2.im = g.part ? rh.y : ro2;
+                bool ok1 = vfinite(r1.re) && vfinite(r1.im), ok2 = vfinite(r2.re) && vfinite(r2.im);
+                for (int t = 0; t < g.cnt; ++t) {
+                    const R y1 = g.part ? q[t].im : q[t].re, y2 = g.part ? q[t].re : q[t].im;
+                    const rpair<R> pa = mul2(r1.re, y1, r1.im, y2);
+                    const rpair<R> pb = mul2(r2.re, y1, r2.im, y2);
+                    const rpair<R> tt = addc2(pa.x, g.part ? pa.y : neg(pa.y), pb.x, g.part ? pb.y : neg(pb.y));
+                    const rpair<R> v = addc2(g.ld_part(c1, g.row0 + t), neg(tt.x), g.ld_part(c2, g.row0 + t),
+                                             neg(tt.y));
+                    if (!vfinite(v.x)) ok1 = false;
+                    if (!vfinite(v.y)) ok2 = false;
+                    g.st_part(c1, g.row0 + t, v.x);
+                    g.st_part(c2, g.row0 + t, v.y);
+                }
+                ok1 = __syncthreads_and(ok1);
+                ok2 = __syncthreads_and(ok2);
+                if (g.tid < 2 && g.crank == 0) {
+                    double* d1 = rdst + ((int64_t)j * n + k) * L2;
+                    double* d2 = (j2 < n) ? rdst + ((int64_t)j2 * n + k) * L2 : ydst + (int64_t)k * L2;
+                    store_real<L>(d1 + g.part * L, 1, rh.x);
+                    store_real<L>(d2 + g.part * L, 1, rh.y);
+                    if (!ok1 && g.tid == 0) record(pos_k + (j - k), 0, XQR_OVERFLOW);
+                    if (!ok2 && g.tid == 0) record(pos_k + (j2 - k), 0, XQR_OVERFLOW);
+                }
+                if (!(ok1 && ok2) && g.tid == 0) atomicExch(abortw, 1);
+                j = j2;  // the loop's j += G moves past the pair
+                continue;
+            }
             double* c = g.col(j);
             // r_kj = q_k^H a_j (reduction.hpp:45-51): this lane's half of the
             // complex leaf cmul(conj(q), a) (complex.hpp:41-44), operands

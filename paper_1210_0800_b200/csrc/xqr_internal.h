@@ -87,18 +87,30 @@ struct GridParams {
     unsigned long long* trace;  // optional (dev): 4 globaltimer stamps per pivot
     int cs;                     // CTAs per cluster
     int* counters;              // [0] pre-pass arrivals, [1] final arrivals, [2] abort word
+    int pair_bulk;              // xgrid2: update trailing columns two at a time (lockstep)
 };
 
 constexpr int kGridMaxRows = 1024;
-// quad-double (xgrid2.cuh): CTAs per cluster and rows per lane pair.  Two
-// CTAs share each SM; 4-CTA clusters measured best for m = 256 and 512.
+// quad-double (xgrid2.cuh): CTAs per cluster, rows per lane pair, and whether
+// trailing columns are updated two at a time.  Two CTAs share each SM.
+// Measured (tools/trace_single.py, same box): m <= 256 -> clusters of up to
+// 4 CTAs, one row per lane pair; 256 < m <= 512 -> 8-CTA clusters, one row
+// per lane pair, paired bulk updates (13.3 vs 14.1 ms for 4 CTAs x 2 rows:
+// the shorter per-pivot chain wins once the bulk keeps up); m > 512 -> 4 CTAs.
 constexpr int kGrid2PerSM = 2;
-inline void grid_shape(int m, int& cs, int& rpp) {
+inline void grid_shape(int m, int& cs, int& rpp, int& pair) {
+    if (m > 256 && m <= 512) {
+        cs = 8;
+        rpp = 1;
+        pair = 1;
+        return;
+    }
     const int need = (m + 63) / 64;
     cs = 1;
     while (cs < need && cs < 4) cs <<= 1;
     rpp = 1;
     while (cs * 64 * rpp < m) rpp <<= 1;
+    pair = 0;
 }
 // double / double-double (xgrid1.cuh): rows per thread of a 256-thread CTA
 inline int grid1_rows_per_thread(int m) {

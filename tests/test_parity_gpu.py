@@ -467,3 +467,22 @@ def test_grid_shape_boundaries(port, L, m):
         gx, gz = xqr.lsq_solve(a, b)
         assert_same(gx, x, f"x m={m} n={n}")
         assert_same(gz, z, f"z m={m} n={n}")
+
+
+@pytest.mark.parametrize("m,n,force", [(300, 60, None), (512, 45, None), (200, 90, "1")])
+def test_grid_paired_bulk_updates(port, monkeypatch, m, n, force):
+    """xgrid2 updates trailing columns two at a time (lockstep pairs) when a
+    cluster owns more than one: on by default for 256 < m <= 512 (8-CTA
+    clusters, 37 of them: pairs form once n + 1 > 37), forced on for m = 200
+    (4-CTA clusters, 74 of them).  Bitwise against the oracle."""
+    if force:
+        monkeypatch.setenv("XQR_GRID_PAIR", force)
+    a, b = port.gen_system(4, m, n, 1.0, 8100 + m + n)
+    q, r, _ = port.mgs_qr(a)
+    gq, gr = xqr.mgs_qr(a)
+    assert_same(gq, q, "Q")
+    assert_same(gr, r, "R")
+    x, z, _ = port.lsq_solve(a, b)
+    gx, gz = xqr.lsq_solve(a, b)
+    assert_same(gx, x, "x")
+    assert_same(gz, z, "z")
