@@ -89,6 +89,24 @@ struct g2 {
     }
 };
 
+// Local staging area for the cluster's warp partials (up to 8 CTAs x 4 warps
+// x 2 halves x 4 limbs; two columns for the paired tree).
+XB_DEVICE double* g2_stage() {
+    __shared__ double s_stage[2 * 8 * 4 * 2 * 4];
+    return s_stage;
+}
+// stage[(r*kG2Warps + w)*2L + part*L + l] = CTA r's slot[buf][w][part][l]
+template <int L, class G2>
+XB_DEVICE void g2_stage_partials(const G2& g, double* slot_local, int buf, int np, double* stage) {
+    namespace cg = cooperative_groups;
+    constexpr int W = 2 * L;  // doubles per warp partial
+    for (int e = g.tid; e < np * W; e += kG2Threads) {
+        const int r = e / (kG2Warps * W), rem = e % (kG2Warps * W);
+        stage[e] = cg::this_cluster().map_shared_rank(slot_local, r)[buf * kG2Warps * W + rem];
+    }
+    __syncthreads();
+}
+
 // Cluster-wide fixed-order tree.  `acc` = this lane's in-lane partial (rows of
 // its pair; `have` = the pair owns at least one row).  Levels: lane pairs of a
 // warp (shuffle offsets 2, 4, 8, 16), then the cluster's 4*CS warp partials
@@ -113,6 +131,11 @@ XB_DEVICE real_t<L> g2_tree(const g2<L, RPP>& g, real_t<L> acc, double* slot_loc
     const int np = kG2Warps * g.cs;          // warp partials in the cluster
     const int npp = np > 16 ? np / 16 : 1;   // partials per pair (1 or 2)
     const int rows_pp = 16 * RPP;            // rows covered by one warp partial
+    // stage the cluster's partials in local shared memory, one DSMEM load per
+    // thread (every warp reading every remote partial itself queues up
+    // hundreds of DSMEM requests per CTA)
+    double* stage = g2_stage();
+    g2_stage_partials<L>(g, slot_local, buf, np, stage);
     R v = acc;
     int have = 0;
     R st0 = acc;
@@ -121,9 +144,8 @@ XB_DEVICE real_t<L> g2_tree(const g2<L, RPP>& g, real_t<L> acc, double* slot_loc
         if (u >= npp) break;
         const int k = pi * npp + u;
         if (k < np && k * rows_pp < g.m) {
-            const double* rem = cg::this_cluster().map_shared_rank(slot_local, k / kG2Warps);
             R w;
-            load_real<L>(rem + ((buf * kG2Warps + (k % kG2Warps)) * 2 + g.part) * L, 1, w);
+            load_real<L>(stage + (k * 2 + g.part) * L, 1, w);
             if (u == 0) {
                 st0 = w;
                 have = 1;
@@ -172,16 +194,26 @@ XB_DEVICE rpair<real_t<L>> g2_tree2(const g2<L, RPP>& g, rpair<real_t<L>> acc, d
     const int np = kG2Warps * g.cs;
     const int npp = np > 16 ? np / 16 : 1;
     const int rows_pp = 16 * RPP;
+    double* stage = g2_stage();
+    double* stage_b = stage + 8 * kG2Warps * 2 * 4;
+    {
+        constexpr int W = 2 * L;
+        for (int e = g.tid; e < np * W; e += kG2Threads) {
+            const int r = e / (kG2Warps * W), rem = e % (kG2Warps * W);
+            stage[e] = cg::this_cluster().map_shared_rank(slot_a, r)[buf * kG2Warps * W + rem];
+            stage_b[e] = cg::this_cluster().map_shared_rank(slot_b, r)[buf * kG2Warps * W + rem];
+        }
+        __syncthreads();
+    }
     rpair<R> v = acc;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
         if (u >= npp) break;
         const int k = pi * npp + u;
         if (k < np && k * rows_pp < g.m) {
-            const int roff = ((buf * kG2Warps + (k % kG2Warps)) * 2 + g.part) * L;
             R wa, wb;
-            load_real<L>(cg::this_cluster().map_shared_rank(slot_a, k / kG2Warps) + roff, 1, wa);
-            load_real<L>(cg::this_cluster().map_shared_rank(slot_b, k / kG2Warps) + roff, 1, wb);
+            load_real<L>(stage + (k * 2 + g.part) * L, 1, wa);
+            load_real<L>(stage_b + (k * 2 + g.part) * L, 1, wb);
             if (u == 0) {
                 v.x = wa;
                 v.y = wb;
@@ -380,7 +412,12 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
             s_flag = (v >= g.cs && *(volatile int*)abortw == 0) ? 1 : 0;
         }
         cg::this_cluster().sync();
-        if (*cg::this_cluster().map_shared_rank(&s_flag, 0) == 0) {
+        // one DSMEM read per CTA, then a CTA broadcast (every thread reading
+        // rank 0's word at once costs microseconds)
+        __shared__ int s_go;
+        if (g.tid == 0) s_go = *cg::this_cluster().map_shared_rank(&s_flag, 0);
+        __syncthreads();
+        if (s_go == 0) {
             abort = true;
             break;
         }

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--phases", action="store_true", help="finisher phase cycles (back substitution)")
     ap.add_argument("--pivots", action="store_true", help="per-pivot phases of the factorisation")
+    ap.add_argument("--split", action="store_true", help="with --pivots: split the critical update")
     args = ap.parse_args()
     path = os.path.join(tempfile.mkdtemp(), "trace.txt")
     os.environ["XQR_GRID_TRACE"] = path
@@ -50,6 +51,16 @@ def main():
                              cur[6] - cur[5], cur[7] - cur[6], cur[2] - cur[7], cur[2] - prv[2]])
             rows = np.array(rows, dtype=np.float64) / 1e3
             names = ["handoff", "update", "normtree", "sqrt", "recip", "divide", "publish", "pivot"]
+            if args.split:
+                sp = []
+                for j in range(2, n - 1):
+                    cur = T[j]
+                    tt = int(t[j, 16])
+                    if min(cur[0], cur[1], cur[3], tt) == 0:
+                        continue
+                    sp.append([cur[3] - cur[0], tt - cur[3], cur[1] - tt])
+                sp = np.array(sp, dtype=np.float64) / 1e3
+                print("  update split (us): leaf %.1f, tree %.1f, axpy+sync %.1f" % tuple(sp.mean(axis=0)))
             for lo, hi in ((0, len(rows) // 3), (len(rows) // 3, 2 * len(rows) // 3), (2 * len(rows) // 3, len(rows))):
                 avg = rows[lo:hi].mean(axis=0)
                 print(f"  pivots {lo + 2}-{hi + 1}: " + ", ".join(f"{k} {v:.1f}" for k, v in zip(names, avg)) + " us")
