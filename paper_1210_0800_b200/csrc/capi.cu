@@ -140,7 +140,7 @@ size_t grid_scratch_bytes(bool lsq, int limbs, int m, int n) {
     const int ncol = n + (lsq ? 1 : 0);
     return sizeof(double) * (grid_ws_doubles(limbs, m, ncol) + (lsq ? xb::rws_doubles(limbs, n) : 0) +
                              (size_t)ncol * limbs) +
-           sizeof(int) * ((size_t)n + 4) + sizeof(unsigned long long) * (8 * (size_t)(n + 1) + 1) +
+           sizeof(int) * ((size_t)n + 4) + sizeof(unsigned long long) * (16 * (size_t)(n + 1) + 1) +
            8 * 256;
 }
 

@@ -170,7 +170,14 @@ XB_DEVICE real_t<L> g2_tree(const g2<L, RPP>& g, real_t<L> acc, double* slot_loc
 XB_CALL_IF rpair<r4> addc2(const r4 a1, const r4 b1, const r4 a2, const r4 b2) {
     return add2_r4(a1, b1, a2, b2);
 }
-XB_DEVICE rpair<r4> vadd(const rpair<r4>& a, const rpair<r4>& b) { return addc2(a.x, b.x, a.y, b.y); }
+XB_DEVICE rpair<r2> addc2(const r2& a1, const r2& b1, const r2& a2, const r2& b2) {
+    return add2(a1, b1, a2, b2);
+}
+template <class R>
+XB_DEVICE rpair<R> vadd(const rpair<R>& a, const rpair<R>& b) { return addc2(a.x, b.x, a.y, b.y); }
+// the stored part of a reciprocal prefix (recip_t, xarith.cuh)
+XB_DEVICE r2& rc_part(recip_t<r2>& rc) { return rc.x1; }
+XB_DEVICE r4& rc_part(recip_t<r4>& rc) { return rc.x; }
 
 // g2_tree for two columns at once (same pairing, same operands per column);
 // slots: one per column, same double buffering.
@@ -352,7 +359,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
             }
             if (g.lane == 0) {
                 store_real<L>(s_rkk, 1, rkk0);
-                if (!code0) store_real<L>(s_rc, 1, rc0.x);
+                if (!code0) store_real<L>(s_rc, 1, rc_part(rc0));
                 s_code = code0;
             }
         }
@@ -361,7 +368,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
         load_real<L>(s_rkk, 1, rkk);
         const int code = s_code;
         recip_t<R> rc;
-        if (!code) load_real<L>(s_rc, 1, rc.x);
+        if (!code) load_real<L>(s_rc, 1, rc_part(rc));
         if (tr) p.trace[j * 8 + 6] = g2_timer();
         // code is cluster-uniform (same tree, same r_kk in every CTA); an
         // overflow while dividing rows is local: it is recorded and stops the
