@@ -329,7 +329,13 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
         thr = mul(rmake<R>((double)m * real_of<L>::eps), best);
     }
     const bool pre_err = __ldcg(p.key) != kNoError;
-    int* abortw = p.counters + 2;
+    // pivot flags: every CTA of the owner cluster adds 1 once q_j is out, or
+    // kFlagErr + 1 if normalising column j failed in it; published when the
+    // low half reaches cs.  A cluster stops only at a failed pivot's flag, so
+    // every round before it still completes everywhere and the first error
+    // in program order is recorded (an overflow in a bulk update is only
+    // recorded: the column's own normalisation fails later)
+    constexpr int kFlagErr = 0x10000;
     if (p.trace && blockIdx.x == 0 && g.tid == 0) p.trace[n * 8 + 6] = g2_timer();
 
     // normalise column j (owner cluster) and publish it.  Returns false on error.
@@ -387,13 +393,12 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
             if (code || !ok) {
                 record(1 + (long long)j * (ncol + 1), code == XQR_BREAKDOWN ? j + 1 : 0,
                        code ? code : XQR_OVERFLOW);
-                atomicExch(abortw, 1);
             } else if (g.crank == 0) {
                 C d{rkk, rmake<R>(0.0)};
                 store_aos<L>(rdst + ((int64_t)j * n + j) * L2, d);
             }
             __threadfence();
-            g2_red_release(p.flags + j, 1);
+            g2_red_release(p.flags + j, (code || !ok) ? kFlagErr + 1 : 1);
             if (p.trace && g.crank == 0) p.trace[j * 8 + 2] = g2_timer();
         }
         return code == 0;
@@ -401,22 +406,20 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
 
     bool abort = pre_err;
     if (!abort && cid == 0) abort = !normalize_publish(0);
-    if (pre_err && blockIdx.x == 0 && g.tid == 0) atomicExch(abortw, 1);
 
     // ---- MGS rounds ----------------------------------------------------------------
     for (int k = 0; k < n && !abort; ++k) {
         const int j0 = k + 1 + ((cid - (k + 1)) % G + G) % G;
         if (j0 >= ncol) continue;
-        // cluster-uniform decision: rank 0 acquires q_k (or sees the abort
-        // word), the cluster barrier hands the verdict to every CTA
+        // cluster-uniform decision: rank 0 acquires q_k (or its failure), the
+        // cluster barrier hands the verdict to every CTA
         if (g.crank == 0 && g.tid == 0) {
             int v;
             // back off while waiting: dozens of clusters polling the L2 flat
             // out slow down everyone's loads, the critical path first
-            while ((v = *(volatile int*)(p.flags + k)) < g.cs && *(volatile int*)abortw == 0)
-                __nanosleep(64);
+            while (((v = *(volatile int*)(p.flags + k)) & (kFlagErr - 1)) < g.cs) __nanosleep(64);
             __threadfence();  // acquire side (pairs with the publisher's red.release)
-            s_flag = (v >= g.cs && *(volatile int*)abortw == 0) ? 1 : 0;
+            s_flag = v < kFlagErr ? 1 : 0;
         }
         cg::this_cluster().sync();
         // one DSMEM read per CTA, then a CTA broadcast (every thread reading
@@ -483,7 +486,6 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
                     if (!ok1 && g.tid == 0) record(pos_k + (j - k), 0, XQR_OVERFLOW);
                     if (!ok2 && g.tid == 0) record(pos_k + (j2 - k), 0, XQR_OVERFLOW);
                 }
-                if (!(ok1 && ok2) && g.tid == 0) atomicExch(abortw, 1);
                 j = j2;  // the loop's j += G moves past the pair
                 continue;
             }
@@ -520,7 +522,6 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
                 store_real<L>(dst + g.part * L, 1, rh);
                 if (!ok && g.tid == 0) record(pos_k + (j - k), 0, XQR_OVERFLOW);
             }
-            if (!ok && g.tid == 0) atomicExch(abortw, 1);
             if (p.trace && g.tid == 0 && g.crank == 0 && j == k + 1) p.trace[(k + 1) * 8 + 1] = g2_timer();
             if (j == k + 1 && j < n) {
                 if (!normalize_publish(j)) {
