@@ -657,8 +657,16 @@ XB_DEV void add_fast2(const r4& a1, const r4& b1, const r4& a2, const r4& b2, r4
 // merge makes (|H_i| > |T_0| for the lead, pair levels apart, the lead's last
 // limb beating T's next one); the pair order is the reference rule (a first
 // iff |a| > |b|).  Fills m[0..7] and returns whether the pattern holds.
+// tail_ok: an early loop exit (four limbs emitted before all eight are
+// merged) leaves only m6, m7 or m7; the reference then folds a's leftovers
+// before b's, which is the merge order unless m6 is b's and m7 is a's --
+// possible only for S = 1 with b leading and its last pair taken first.
+#ifndef XB_SHIFT_TAIL
+#define XB_SHIFT_TAIL 0
+#endif
 template <int S>
-XB_DEV bool shift_merge(const r4& H, const r4& T, bool h_is_a, double (&m)[8]) {
+XB_DEV bool shift_merge(const r4& H, const r4& T, bool h_is_a, double (&m)[8], bool& tail_ok) {
+    tail_ok = true;
     const double h[4] = {H.c0, H.c1, H.c2, H.c3}, t[4] = {T.c0, T.c1, T.c2, T.c3};
     bool ok = true;
 #pragma unroll
@@ -680,6 +688,7 @@ XB_DEV bool shift_merge(const r4& H, const r4& T, bool h_is_a, double (&m)[8]) {
         if (l + S == 3) {
             // after the last pair: if T's limb went first, H_3 must beat T_{4-S}
             ok = ok && (hfirst || (dabs(hh) > dabs(t[4 - S])));
+            if (S == 1) tail_ok = h_is_a || hfirst;
         }
     }
 #pragma unroll
@@ -728,10 +737,16 @@ XB_DEV r4 add_alt_fast(const r4& a, const r4& b, bool& okr) {
         const bool alead = f0;
         const r4& H = alead ? a : b;
         const r4& T = alead ? b : a;
-        bool hit = shift_merge<2>(H, T, alead, mm);
-        if (!hit) hit = shift_merge<1>(H, T, alead, mm);
-        if (!hit) hit = shift_merge<3>(H, T, alead, mm);
+        bool tail_ok;
+        bool hit = shift_merge<2>(H, T, alead, mm, tail_ok);
+        if (!hit) hit = shift_merge<1>(H, T, alead, mm, tail_ok);
+        if (!hit) hit = shift_merge<3>(H, T, alead, mm, tail_ok);
         if (hit) {
+            // XB_SHIFT_TAIL: fold leftovers in place after an early exit (the
+            // single-system kernels, whose Newton chains hit it ~25 % of the
+            // time); off elsewhere -- the batched kernel is faster without
+            // the extra live state in its call-form helpers
+            q.tail = XB_SHIFT_TAIL ? tail_ok : false;
             m0 = mm[0];
             m1 = mm[1];
             q.m2 = mm[2];

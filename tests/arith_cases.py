@@ -14,7 +14,10 @@ of quick_three_accum and of both renorm trees):
 * sparse: random limbs zeroed (zeros inside the limb sequence);
 * ties: equal magnitudes, opposite signs, signed zeros;
 * dyadic: short-mantissa limbs spaced ~54 bits apart, so partial sums are
-  exact and zero error terms appear inside otherwise regular merges.
+  exact and zero error terms appear inside otherwise regular merges;
+* newton: x and a correction 1-3 limbs below it (x + x*(1 - b*x) and the
+  sqrt/division corrections), either operand first -- the shifted merges,
+  including the ones whose loop exits early and folds leftovers.
 """
 import numpy as np
 
@@ -33,7 +36,7 @@ def random_operands(rng, count, L, emin=-40, emax=40, parts=1):
 def operand_pairs(rng, count, L, renorm, parts=1):
     """(a, b) arrays of shape (count, parts, L) mixing all classes; `renorm`
     renormalises an (N, L) array (the oracle's op 8)."""
-    per = count // 7
+    per = count // 8
     a = random_operands(rng, count, L, parts=parts)
     b = random_operands(rng, count, L, parts=parts)
     if L > 1:
@@ -82,4 +85,16 @@ def operand_pairs(rng, count, L, renorm, parts=1):
         sg = np.where(rng.random((per, parts, L)) < 0.5, -1.0, 1.0)
         gaps = np.cumsum(rng.integers(53, 57, size=(per, parts, L)), axis=-1) - 53
         arr[s:s + per] = sg * np.ldexp(mant, e0[..., None] - gaps)
+    s += per
+    # newton: b = a correction S limbs (54 S bits, +-4) below a, either order
+    if L > 1:
+        c = random_operands(rng, per, L, -2, 2, parts)
+        c = renorm(c.reshape(-1, L)).reshape(c.shape)
+        shift = 54 * rng.integers(1, 4, size=(per, parts, 1)) + rng.integers(-4, 5, size=(per, parts, 1))
+        sg = np.where(rng.random((per, parts, 1)) < 0.5, -1.0, 1.0)
+        b[s:s + per] = sg * np.ldexp(c, -shift)
+        sw = rng.random(per) < 0.5
+        tmp = a[s:s + per][sw].copy()
+        a[s:s + per][sw] = b[s:s + per][sw]
+        b[s:s + per][sw] = tmp
     return np.ascontiguousarray(a), np.ascontiguousarray(b)
