@@ -36,7 +36,15 @@ def main():
         last = t[-1]
         start, grid_end, bs_start, bs_end = int(last[8]), int(last[5]), int(last[6]), int(last[7])
         fact = (grid_end - start) / 1e3 if start else float("nan")
-        if args.pivots:
+        if args.pivots and args.limbs <= 2:
+            # xgrid1 stamps: 0 q_{j-1} in hand, 1 column j updated, 2 published
+            T = t[:, 1:9].astype(np.int64)
+            rows = [[T[j][0] - T[j - 1][2], T[j][1] - T[j][0], T[j][2] - T[j][1]]
+                    for j in range(2, args.n - 1) if min(T[j][0], T[j][1], T[j][2], T[j - 1][2]) > 0]
+            if rows:
+                avg = np.array(rows, dtype=np.float64).mean(axis=0) / 1e3
+                print("  dd pivots: handoff %.2f, update %.2f, normalise+publish %.2f us" % tuple(avg))
+        elif args.pivots:
             # per pivot j (row j of the trace, globaltimer ns): 0 q_{j-1} in hand,
             # 1 column j updated, 4 norm tree, 5 sqrt, 6 reciprocal, 7 divided,
             # 2 published; 3 last cluster done with round j-1
