@@ -486,3 +486,49 @@ def test_grid_paired_bulk_updates(port, monkeypatch, m, n, force):
     gx, gz = xqr.lsq_solve(a, b)
     assert_same(gx, x, "x")
     assert_same(gz, z, "z")
+
+
+# ---- the reference's known answers (test_mgs.cpp) through the device ------------------
+@pytest.mark.parametrize("L", [1, 2, 4])
+@pytest.mark.parametrize("n", [4, 64, 200])
+def test_known_answer_identity_device(L, n):
+    """test_mgs.cpp:45-55 (identity factors to identity) at the CTA size and
+    at grid-kernel sizes; lsq_solve on I returns b with z = 0 (:220-228)."""
+    a = np.zeros((n, n, 2, L))
+    for k in range(n):
+        a[k, k, 0, 0] = 1.0
+    q, r = xqr.mgs_qr(a)
+    assert_same(q, a, "Q")
+    assert_same(r, a, "R")
+    rng = np.random.default_rng(n + L)
+    b = np.zeros((n, 2, L))
+    b[..., 0] = rng.uniform(-1, 1, (n, 2))
+    x, z = xqr.lsq_solve(a, b)
+    assert_same(x, b, "x")
+    assert not np.any(z.view(np.uint64)), "z must be +0"
+
+
+@pytest.mark.parametrize("L", [1, 2, 4])
+@pytest.mark.parametrize("n", [2, 64])
+def test_known_answer_breakdowns_device(L, n):
+    """test_mgs.cpp:70-90: a zero matrix breaks down at column 1; a repeated
+    column at its (1-based) index -- on the CTA and the grid kernels."""
+    with pytest.raises(xqr.breakdown_error) as e:
+        xqr.mgs_qr(np.zeros((n, n, 2, L)))
+    assert e.value.column == 1
+    a = np.zeros((n, n, 2, L))
+    rng = np.random.default_rng(3)
+    a[..., 0] = rng.uniform(-1, 1, (n, n, 2))
+    a[1] = a[0]
+    with pytest.raises(xqr.breakdown_error) as e:
+        xqr.mgs_qr(a)
+    assert e.value.column == 2
+
+
+def test_known_answer_three_four_five_device():
+    """test_mgs.cpp:57-68: (3, 4) normalises exactly to r = 5, q = (0.6, 0.8)."""
+    a = np.zeros((1, 2, 2, 1))
+    a[0, 0, 0, 0], a[0, 1, 0, 0] = 3.0, 4.0
+    q, r = xqr.mgs_qr(a)
+    assert r[0, 0, 0, 0] == 5.0 and r[0, 0, 1, 0] == 0.0
+    assert q[0, 0, 0, 0] == 0.6 and q[0, 1, 0, 0] == 0.8
