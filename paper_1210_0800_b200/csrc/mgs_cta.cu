@@ -47,7 +47,8 @@ __global__ void __launch_bounds__(512, 1) flow_backsub_kernel(BackSubParams p) {
 template <int L>
 static cudaError_t launch_bs(const BackSubParams& p, cudaStream_t s) {
     const size_t flow_smem = sizeof(double) * (size_t)p.n * (5 * L + 1);
-    if (p.batch == 1 && flow_smem <= 200 * 1024) {
+    // (quad-double only: double-double steps are too short to gain from it)
+    if (L == 4 && p.batch == 1 && flow_smem <= 200 * 1024) {
         auto kern = flow_backsub_kernel<L>;
         if (flow_smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -192,113 +192,11 @@ XB_DEVICE bool cta_back_substitute(int n, const double* r, const double* y, doub
     return false;
 }
 
-// Latency-first form for the single-system quad-double kernel (xgrid2.cuh):
-// a LANE PAIR owns unknowns j = pair, pair + P, ... (P = blockDim.x / 2) and
-// splits every complex operation into its real half (even lane) and
-// imaginary half (odd lane) -- the halves of cmul / csub / the Smith
-// quotient are independent (complex.hpp:41-58).  Per step k
-// (mgs.hpp:117-124): x_j -= r_jk * x_k for j < k, the owner of k-1 first, and
-// the owner of x_{k-1} divides it at once (look-ahead).  R-only Smith parts
-// come from cta_backsub_prep.  Same operations, operands and order as the
-// reference; returns (uniformly) true on error.
-template <int L>
-XB_DEVICE bool pair_back_substitute(int n, const double* r, const double* y, double* xs, double* prep,
-                                    unsigned long long* key, long long pos_base) {
-    using R = real_t<L>;
-    const int tid = threadIdx.x, P = blockDim.x / 2, pair = tid >> 1, part = tid & 1;
-    const unsigned pmask = 3u << (tid & 30);  // this lane pair
-    cta_backsub_prep<L>(n, r, y, xs, prep);
-    __syncthreads();
-    bool err = false;
-    // own half of x_j = x_j / d_j (complex.hpp:50-57) given both halves of x_j
-    auto smith = [&](const R& are, const R& aim, int j) -> R {
-        const smith_prep<L> sp = prep_load<L>(prep + (size_t)j * (3 * L + 1));
-        R num;
-        if (sp.br) {  // a.re + a.im*t  |  a.im - a.re*t
-            const R prod = mul(part ? are : aim, sp.t);
-            num = add(part ? aim : are, part ? neg(prod) : prod);
-        } else {      // a.re*t + a.im  |  a.im*t - a.re
-            const R prod = mul(part ? aim : are, sp.t);
-            num = add(prod, part ? neg(are) : aim);
-        }
-        return divide(num, sp.d, sp.rc);
-    };
-    auto xs_part = [&](int j, int pp) { return xs + (size_t)j * 2 * L + pp * L; };
-    // last unknown
-    if (pair == (n - 1) % P) {
-        const smith_prep<L> sp = prep_load<L>(prep + (size_t)(n - 1) * (3 * L + 1));
-        R are, aim;
-        load_real<L>(xs_part(n - 1, 0), 1, are);
-        load_real<L>(xs_part(n - 1, 1), 1, aim);
-        R v = part ? aim : are;
-        if (sp.code) {
-            if (part == 0) atomicMin(key, status_key(pos_base, 0, sp.code));
-            err = true;
-        } else {
-            v = smith(are, aim, n - 1);
-            if (!vfinite(v) || !vfinite(shfl_pair(v, pmask))) {
-                if (part == 0) atomicMin(key, status_key(pos_base, 0, 2));
-                err = true;
-            }
-        }
-        store_real<L>(xs_part(n - 1, part), 1, v);
-    }
-    if (__syncthreads_or(err)) return true;
-    for (int k = n - 1; k >= 1; --k) {
-        R xkre, xkim;
-        load_real<L>(xs_part(k, 0), 1, xkre);
-        load_real<L>(xs_part(k, 1), 1, xkim);
-        const double* rk = r + (size_t)k * n * 2 * L;
-        // highest owned j < k first: the owner of k-1 reaches its division soonest
-        int j = pair + ((k - 1 - pair) / P) * P;
-        if (k - 1 < pair) j = -1;
-        for (; j >= 0; j -= P) {
-            R rre, rim, xj;
-            load_real<L>(rk + (size_t)j * 2 * L, 1, rre);
-            load_real<L>(rk + (size_t)j * 2 * L + L, 1, rim);
-            load_real<L>(xs_part(j, part), 1, xj);
-            // t = cmul(r_jk, x_k) (complex.hpp:41-44): own half
-            const R y1 = part ? xkim : xkre, y2 = part ? xkre : xkim;
-            rpair<R> pr = mul2(rre, y1, rim, y2);
-            const R t = add(pr.x, part ? pr.y : neg(pr.y));
-            R v = sub(xj, t);  // csub (complex.hpp:31-34)
-            bool bad = !vfinite(v) || !vfinite(shfl_pair(v, pmask));
-            if (bad) {
-                if (part == 0) atomicMin(key, status_key(pos_base + (n - 1 - k), 0, 2));
-                err = true;
-            } else if (j == k - 1) {
-                const smith_prep<L> sp = prep_load<L>(prep + (size_t)j * (3 * L + 1));
-                if (sp.code) {
-                    if (part == 0) atomicMin(key, status_key(pos_base + (n - k), 0, sp.code));
-                    err = true;
-                } else {
-                    const R o = shfl_pair(v, pmask);
-                    v = smith(part ? o : v, part ? v : o, j);
-                    if (!vfinite(v) || !vfinite(shfl_pair(v, pmask))) {
-                        if (part == 0) atomicMin(key, status_key(pos_base + (n - k), 0, 2));
-                        err = true;
-                    }
-                }
-            }
-            store_real<L>(xs_part(j, part), 1, v);
-        }
-        // R is known from the start: pull next step's r_{j,k-1} (and the
-        // next pivot's Smith record) into L1 while the barrier drains
-        if (k >= 2) {
-            const double* rn = r + (size_t)(k - 1) * n * 2 * L;
-            for (int jj = pair; jj < k - 1; jj += P)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(rn + (size_t)jj * 2 * L + part * L));
-            if (tid == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(prep + (size_t)(k - 2) * (3 * L + 1)));
-        }
-        if (__syncthreads_or(err)) return true;
-    }
-    return false;
-}
-
-
-// Warp-specialised form of pair_back_substitute for one system (same
-// lane-pair split, same operations and order per unknown, mgs.hpp:117-124),
-// without a CTA barrier per step.  The sequential chain of the column sweep is
+// Warp-specialised back substitution of one system (mgs.hpp:117-124): a
+// LANE PAIR owns an unknown and splits every complex operation into its real
+// half (even lane) and imaginary half (odd lane) -- the halves of cmul / csub
+// / the Smith quotient are independent (complex.hpp:41-58) -- and there is no
+// CTA barrier per step.  The sequential chain of the column sweep is
 //   x_k final -> x_{k-1} -= r_{k-1,k} x_k -> Smith division of x_{k-1},
 // and every other update x_j -= r_jk x_k (j <= k-2) can run a step or more
 // behind it.  So:
