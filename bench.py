@@ -232,12 +232,20 @@ def main():
 
     import paper_1210_0800_b200 as xqr
 
+    # one GPU per rank; BENCH_DIST_BACKEND=gloo (dev) lets a one-GPU box run
+    # the N > 1 code path with every rank on the same device
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dist = None
+    red_dev = "cuda" if backend == "nccl" else "cpu"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_1210_0800_b200.sharding import max_over_ranks, shard
 
     limbs, m, n = 4, args.m, args.n
@@ -283,7 +291,7 @@ def main():
     launches = ctx.launch_count - launches0
     ms = e0.elapsed_time(e1)
     last_kernel_ms = ctx.last_kernel_ms  # CUDA events around the last launch, ctx stream
-    ms = max_over_ranks(ms, dist, "cuda")
+    ms = max_over_ranks(ms, dist, red_dev)
     total = (args.batch * world if args.scaling == "weak" else args.batch) * args.steps
     value = total / (ms / 1e3)
 
@@ -313,7 +321,7 @@ def main():
         xh, zh, ch, _ = xqr.lsq_solve_batched(a_pin, b_pin, device=local)
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-    e2e_s = max_over_ranks(e2e_s, dist, "cuda")
+    e2e_s = max_over_ranks(e2e_s, dist, red_dev)
     e2e_value = (args.batch * world if args.scaling == "weak" else args.batch) / e2e_s
     h2d = a.nbytes + b.nbytes
     d2h = xh.nbytes + zh.nbytes + 16 * per_rank
