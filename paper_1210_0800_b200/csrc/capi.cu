@@ -128,7 +128,11 @@ bool use_grid_path(xqr_ctx* ctx, int limbs, int m, int n) {
     // quad-double pivots are slow enough that even a small system gains from
     // spreading its columns over SMs; double-double needs a larger one
     if (limbs == 4) return ctx->coop && n >= 4 && m >= 16 && m <= xb::kGridMaxRows;
-    return ctx->coop && n >= 8 && m >= 64 && m <= xb::kGridMaxRows;
+    // (measured, tools/small_latency.py: cdd 32x32 207 vs 284 us on one CTA,
+    // 48x48 302 vs 739; 16x16 114 vs 104)
+    int min_m = 32;
+    if (const char* e = std::getenv("XQR_DD_GRID_MIN_M")) min_m = std::atoi(e);  // dev
+    return ctx->coop && n >= 8 && m >= min_m && m <= xb::kGridMaxRows;
 }
 
 size_t grid_ws_doubles(int limbs, int m, int ncol) {

@@ -8,7 +8,7 @@ import numpy as np, torch
 import paper_1210_0800_b200 as xqr
 ctx = xqr.context(0)
 s = torch.cuda.Stream(); torch.cuda.set_stream(s); ctx.set_stream(s.cuda_stream)
-for L, m, n in ((4, 16, 16), (4, 32, 32), (4, 48, 48), (4, 64, 64), (4, 80, 80), (2, 64, 64), (2, 128, 128)):
+for L, m, n in [tuple(int(v) for v in c.split(",")) for c in (sys.argv[1:] or ["4,16,16", "4,32,32", "4,48,48", "4,64,64", "4,80,80", "2,64,64", "2,128,128"])]:
     a, b = xqr.gen_systems(L, 1, m, n, 1.0, 1, -1)
     da = torch.from_numpy(a).cuda(); db = torch.from_numpy(b).cuda()
     dx = torch.zeros((1, n, 2, L), dtype=torch.float64, device="cuda"); dz = torch.zeros((1, L), dtype=torch.float64, device="cuda")
