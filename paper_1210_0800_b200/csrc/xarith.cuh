@@ -1084,6 +1084,20 @@ XB_DEV r4 divide(const r4& a, const r4& b, const recip_t<r4>& rc) {
     return addz(q, mulc(rc.x, subc(a, mulc(b, q))));
 }
 
+// divide() with its five operations inline instead of the shared call
+// forms (same operations, same bits): faster where the surrounding code is
+// small enough to stay in the instruction cache (the back-substitution step)
+XB_DEV r4 divide_inline(const r4& a, const r4& b, const recip_t<r4>& rc) {
+    const r4 q = mul(a, rc.x);
+    const r4 c = mul(rc.x, add(a, neg(mul(b, q))));
+    bool ok;
+    r4 out = add_alt_fast(q, c, ok);  // addz: the correction sits limbs below q
+    if (!ok) out = add(q, c);
+    return out;
+}
+XB_DEV r2 divide_inline(const r2& a, const r2& b, const recip_t<r2>& rc) { return divide(a, b, rc); }
+XB_DEV r1 divide_inline(const r1& a, const r1& b, const recip_t<r1>& rc) { return divide(a, b, rc); }
+
 template <class R>
 XB_DEV R rdiv(const R& a, const R& b, int& status) {
     recip_t<R> rc = recip(b, status);

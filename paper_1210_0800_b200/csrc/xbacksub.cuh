@@ -258,7 +258,7 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
             const R prod = mul(part ? aim : are, sp.t);
             num = add(prod, part ? neg(are) : aim);
         }
-        return divide(num, sp.d, sp.rc);
+        return divide_inline(num, sp.d, sp.rc);
     };
     // own half of x_j - r_jk x_k (cmul complex.hpp:41-44, csub :31-34), given
     // this lane's (y1, y2) = (x_k.re, x_k.im) or (x_k.im, x_k.re)
