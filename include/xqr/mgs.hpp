@@ -171,7 +171,7 @@ lsq_batch_result<R> lsq_solve_batched(const std::vector<col_matrix<R>>& a,
     int rc = xqr_lsq_solve_batched(device::context(), device::limbs<R>(), (int64_t)a.size(),
                                    (int64_t)m, (int64_t)n, ain.data(), bin.data(), x.data(), z.data(),
                                    st.data());
-    if (rc >= XQR_USAGE) device::raise_status(rc, st[0]);
+    if (rc >= XQR_DIMENSION) device::raise_status(rc, st[0]);  // shape / usage / device: the whole call
     out.solutions.resize(a.size(), lsq_solution<R>{cvector<R>(n), R(0.0)});
     for (std::size_t s = 0; s < a.size(); ++s) {
         std::memcpy(out.solutions[s].x.data(), x.data() + s * n * e, n * e * sizeof(double));

@@ -363,7 +363,7 @@ def residual_max_entry_batched(a, q, r, device: int = 0):
     st = (xqr_status * max(batch, 1))()
     rc = ctx._lib.xqr_residual_max_entry_batched(ctx.handle, L, batch, m, n, pa, pq, pr,
                                                  out.ctypes.data_as(_dp), st)
-    if rc >= XQR_USAGE:
+    if rc >= XQR_DIMENSION:  # shape, usage, device: the whole call
         _raise(rc, 0, ctx.last_error())
     return out, np.array([st[i].code for i in range(batch)], dtype=np.int32)
 
@@ -376,7 +376,7 @@ def orthogonality_defect_batched(q, device: int = 0):
     st = (xqr_status * max(batch, 1))()
     rc = ctx._lib.xqr_orthogonality_defect_batched(ctx.handle, L, batch, m, n, pq,
                                                    out.ctypes.data_as(_dp), st)
-    if rc >= XQR_USAGE:
+    if rc >= XQR_DIMENSION:  # shape, usage, device: the whole call
         _raise(rc, 0, ctx.last_error())
     return out, np.array([st[i].code for i in range(batch)], dtype=np.int32)
 
@@ -423,7 +423,7 @@ def lsq_solve_batched(a, b, device: int = 0, raise_first: bool = False):
                                         z.ctypes.data_as(_dp), st)
     codes = np.array([st[i].code for i in range(batch)], dtype=np.int32)
     cols = np.array([st[i].column for i in range(batch)], dtype=np.int32)
-    if rc and (raise_first or rc >= XQR_USAGE):
+    if rc and (raise_first or rc >= XQR_DIMENSION):  # shape, usage, device: the whole call
         i = int(np.nonzero(codes)[0][0]) if codes.any() else 0
         _raise(rc, int(cols[i]) if batch else 0, ctx.last_error())
     return x, z, codes, cols
@@ -441,7 +441,7 @@ def mgs_qr_batched(a, device: int = 0, raise_first: bool = False):
                                      r.ctypes.data_as(_dp), st)
     codes = np.array([st[i].code for i in range(batch)], dtype=np.int32)
     cols = np.array([st[i].column for i in range(batch)], dtype=np.int32)
-    if rc and (raise_first or rc >= XQR_USAGE):
+    if rc and (raise_first or rc >= XQR_DIMENSION):  # shape, usage, device: the whole call
         i = int(np.nonzero(codes)[0][0]) if codes.any() else 0
         _raise(rc, int(cols[i]) if batch else 0, ctx.last_error())
     return q, r, codes, cols

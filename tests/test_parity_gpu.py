@@ -532,3 +532,20 @@ def test_known_answer_three_four_five_device():
     q, r = xqr.mgs_qr(a)
     assert r[0, 0, 0, 0] == 5.0 and r[0, 0, 1, 0] == 0.0
     assert q[0, 0, 0, 0] == 0.6 and q[0, 1, 0, 0] == 0.8
+
+
+@pytest.mark.parametrize("L", [1, 2, 4])
+@pytest.mark.parametrize("m,n", [(3, 5), (3, 0), (0, 0), (16, 17), (64, 65)])
+def test_dimension_errors_device(port, L, m, n):
+    """Shapes the reference rejects with dimension_error (mgs.hpp, matrix.hpp:
+    m < n, empty) are rejected the same way by the device API, single and
+    batched, including sizes that would otherwise route to the grid kernels."""
+    a = np.zeros((n, m, 2, L))
+    b = np.zeros((m, 2, L))
+    assert port.mgs_qr(a)[2][0] == 4 and port.lsq_solve(a, b)[2][0] == 4
+    with pytest.raises(xqr.dimension_error):
+        xqr.mgs_qr(a)
+    with pytest.raises(xqr.dimension_error):
+        xqr.lsq_solve(a, b)
+    with pytest.raises(xqr.dimension_error):
+        xqr.lsq_solve_batched(a[None], b[None])
