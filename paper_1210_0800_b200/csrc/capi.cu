@@ -433,7 +433,9 @@ int solve_host_batched(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t
                        xqr_status* st) {
     const size_t L2 = 2 * (size_t)limbs;
     const int ncol = (int)n + (lsq ? 1 : 0);
-    int64_t chunk = 4 * (int64_t)ctx->num_sms;
+    // one kernel wave per chunk (quad-double m <= 128: 2 CTAs per SM, else 4):
+    // the first chunk's copy is the only one not hidden behind a solve
+    int64_t chunk = (limbs == 4 && m <= 128 ? 2 : 4) * (int64_t)ctx->num_sms;
     if (const char* e = std::getenv("XQR_CHUNK")) chunk = std::max<int64_t>(1, std::atoll(e));
     if (chunk > batch) chunk = batch;
     const int64_t nchunks = (batch + chunk - 1) / chunk;
