@@ -218,7 +218,7 @@ def test_cd_overflow_propagates(port):
 
 
 @pytest.mark.parametrize("L", [2, 4])
-@pytest.mark.parametrize("m,n", [(70, 20), (24, 12)])
+@pytest.mark.parametrize("m,n", [(70, 20), (24, 12), (300, 50)])
 def test_single_system_grid_error_paths(port, L, m, n):
     """The whole-GPU single-system kernels (xgrid1 for dd, m >= 64; xgrid2 for
     qd, m >= 16) report the reference's first error: a breakdown in the middle
