@@ -113,8 +113,9 @@ int check_shape(xqr_ctx* ctx, xqr_status* st, int limbs, int64_t batch, int64_t 
     if (!valid_limbs(limbs)) return fail(ctx, st, XQR_USAGE, "limbs must be 1, 2 or 4");
     if (n < 1 || m < n) return fail(ctx, st, XQR_DIMENSION, "matrix shape must satisfy rows >= cols >= 1");
     if (batch < 0) return fail(ctx, st, XQR_USAGE, "negative batch");
-    if (m > 32 * xb::kMaxRowsPerLane)
-        return fail(ctx, st, XQR_USAGE, "rows > 1024 not supported by this build");
+    if (m > xb::kGridMaxRows) return fail(ctx, st, XQR_USAGE, "rows > 2048 not supported by this build");
+    if (m > 32 * xb::kMaxRowsPerLane && batch != 1)
+        return fail(ctx, st, XQR_USAGE, "batched systems with rows > 1024 not supported by this build");
     if (batch > 0x7fffffff) return fail(ctx, st, XQR_USAGE, "batch too large");
     return 0;
 }
@@ -127,6 +128,7 @@ bool use_grid_path(xqr_ctx* ctx, int limbs, int m, int n) {
     }
     // quad-double pivots are slow enough that even a small system gains from
     // spreading its columns over SMs; double-double needs a larger one
+    if (m > 32 * xb::kMaxRowsPerLane) return true;  // only the grid kernels take m > 1024
     if (limbs == 4) return ctx->coop && n >= 4 && m >= 16 && m <= xb::kGridMaxRows;
     // (measured, tools/small_latency.py: cdd 32x32 207 vs 284 us on one CTA,
     // 48x48 302 vs 739; 16x16 114 vs 104)

@@ -153,10 +153,13 @@ cudaError_t launch_metric_t(int which, int64_t batch, int m, int n, const double
         const int64_t npairs = (int64_t)n * (n + 1) / 2;
         nblocks = (int)((npairs + 7) / 8);
         const int rpl = rows_per_lane(m);
+        // in-lane tree depth: the binary counter holds up to 2^LV - 1 leaves
         if (rpl <= 4)
             orthodefect_kernel<L, 3><<<dim3(nblocks, (unsigned)batch), 256, 0, s>>>(m, n, rpl, q, part, flags);
-        else
+        else if (rpl <= 32)
             orthodefect_kernel<L, 6><<<dim3(nblocks, (unsigned)batch), 256, 0, s>>>(m, n, rpl, q, part, flags);
+        else
+            orthodefect_kernel<L, 7><<<dim3(nblocks, (unsigned)batch), 256, 0, s>>>(m, n, rpl, q, part, flags);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

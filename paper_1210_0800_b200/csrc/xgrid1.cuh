@@ -359,7 +359,8 @@ namespace xb {
 
 template <int L, bool LSQ>
 cudaError_t launch_grid1(const GridParams& p, int grid, cudaStream_t s) {
-    auto kern = mgs_grid_kernel<L, 3, LSQ>;
+    // rows per thread <= 4: a 3-level in-thread tree; 8 (m <= 2048): 4 levels
+    auto kern = p.rpt <= 4 ? mgs_grid_kernel<L, 3, LSQ> : mgs_grid_kernel<L, 4, LSQ>;
     const size_t smem = sizeof(double) * 2 * L * kGridThreads * p.rpt;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

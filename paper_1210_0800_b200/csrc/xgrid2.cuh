@@ -578,8 +578,12 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
 // chain, updater warps trail it; no CTA barrier per step.
 constexpr int kG2BsThreads = 512;
 template <int L>
-constexpr size_t g2_backsub_smem(int n) {
-    return sizeof(double) * (size_t)n * (2 * L + 3 * L + 1);
+__host__ __device__ constexpr bool g2_backsub_prep_in_smem(int n) {
+    return sizeof(double) * (size_t)n * (2 * L + 3 * L + 1) <= 200 * 1024;
+}
+template <int L>
+__host__ __device__ constexpr size_t g2_backsub_smem(int n) {
+    return sizeof(double) * (size_t)n * (g2_backsub_prep_in_smem<L>(n) ? 2 * L + 3 * L + 1 : 2 * L);
 }
 template <int L>
 __global__ void __launch_bounds__(kG2BsThreads, 1) grid2_backsub_kernel(GridParams p) {
@@ -593,7 +597,9 @@ __global__ void __launch_bounds__(kG2BsThreads, 1) grid2_backsub_kernel(GridPara
     if (s_key != kNoError) return;  // status already written by the factorisation
     if (p.trace && threadIdx.x == 0) p.trace[n * 8 + 5] = g2_timer();
     const double* ydst = p.rws + (int64_t)n * n * L2;
-    double* prep = xs + (size_t)n * L2;
+    // the Smith records in shared memory when they fit, else in the global
+    // scratch after y (n > ~1300 quad-double unknowns)
+    double* prep = g2_backsub_prep_in_smem<L>(n) ? xs + (size_t)n * L2 : p.rws + (int64_t)n * n * L2 + (int64_t)n * L2;
     bool bad = flow_back_substitute<L>(n, p.rws, ydst, xs, prep, s_sync, &s_key,
                                        2 + (long long)n * (ncol + 1), p.trace ? p.trace + 8 * (n + 1) : nullptr);
     if (!bad)

@@ -90,7 +90,9 @@ struct GridParams {
     int pair_bulk;              // xgrid2: update trailing columns two at a time (lockstep)
 };
 
-constexpr int kGridMaxRows = 1024;
+// single systems (the grid kernels) take m <= kGridMaxRows; batches (one CTA
+// per system) m <= 32 * kMaxRowsPerLane
+constexpr int kGridMaxRows = 2048;
 // quad-double (xgrid2.cuh): CTAs per cluster, rows per lane pair, and whether
 // trailing columns are updated two at a time.  Two CTAs share each SM.
 // Measured (tools/trace_single.py, same box): m <= 256 -> clusters of up to
@@ -103,6 +105,12 @@ inline void grid_shape(int m, int& cs, int& rpp, int& pair) {
         cs = 8;
         rpp = 1;
         pair = 1;
+        return;
+    }
+    if (m > 1024) {  // up to kGridMaxRows = 2048: 8 CTAs x 64 lane pairs x 4 rows
+        cs = 8;
+        rpp = 4;
+        pair = 0;
         return;
     }
     const int need = (m + 63) / 64;

@@ -490,7 +490,7 @@ def test_grid_paired_bulk_updates(port, monkeypatch, m, n, force):
 
 # ---- the reference's known answers (test_mgs.cpp) through the device ------------------
 @pytest.mark.parametrize("L", [1, 2, 4])
-@pytest.mark.parametrize("n", [4, 64, 200])
+@pytest.mark.parametrize("n", [4, 64, 200, 1100, 1400])
 def test_known_answer_identity_device(L, n):
     """test_mgs.cpp:45-55 (identity factors to identity) at the CTA size and
     at grid-kernel sizes; lsq_solve on I returns b with z = 0 (:220-228)."""
@@ -549,3 +549,26 @@ def test_dimension_errors_device(port, L, m, n):
         xqr.lsq_solve(a, b)
     with pytest.raises(xqr.dimension_error):
         xqr.lsq_solve_batched(a[None], b[None])
+
+
+# ---- single systems beyond 1024 rows (grid kernels only) ------------------------------
+@pytest.mark.parametrize("L,m", [(4, 1025), (4, 1500), (4, 2048), (2, 1025), (2, 2048), (1, 1300)])
+def test_tall_single_systems(port, L, m):
+    """m in (1024, 2048]: qd on 8-CTA clusters with 4 rows per lane pair, dd / d
+    on the CTA-per-column kernel with 8 rows per thread; bitwise, plus the
+    device metrics.  Batches of such systems are refused (one CTA per system
+    holds at most 1024 rows)."""
+    for n in (3, 9):
+        a, b = port.gen_system(L, m, n, 1.0, 9100 + m + n)
+        q, r, _ = port.mgs_qr(a)
+        gq, gr = xqr.mgs_qr(a)
+        assert_same(gq, q, f"Q m={m} n={n}")
+        assert_same(gr, r, f"R m={m} n={n}")
+        x, z, _ = port.lsq_solve(a, b)
+        gx, gz = xqr.lsq_solve(a, b)
+        assert_same(gx, x, f"x m={m} n={n}")
+        assert_same(gz, z, f"z m={m} n={n}")
+        assert_same(xqr.residual_max_entry(a, q, r), port.residual_max_entry(a, q, r)[0], "residual")
+        assert_same(xqr.orthogonality_defect(q), port.orthogonality_defect(q)[0], "orthogonality")
+    with pytest.raises(xqr.usage_error):
+        xqr.lsq_solve_batched(a[None].repeat(2, 0), b[None].repeat(2, 0))
