@@ -114,8 +114,6 @@ int check_shape(xqr_ctx* ctx, xqr_status* st, int limbs, int64_t batch, int64_t 
     if (n < 1 || m < n) return fail(ctx, st, XQR_DIMENSION, "matrix shape must satisfy rows >= cols >= 1");
     if (batch < 0) return fail(ctx, st, XQR_USAGE, "negative batch");
     if (m > xb::kGridMaxRows) return fail(ctx, st, XQR_USAGE, "rows > 2048 not supported by this build");
-    if (m > 32 * xb::kMaxRowsPerLane && batch != 1)
-        return fail(ctx, st, XQR_USAGE, "batched systems with rows > 1024 not supported by this build");
     if (batch > 0x7fffffff) return fail(ctx, st, XQR_USAGE, "batch too large");
     return 0;
 }
@@ -152,9 +150,10 @@ size_t grid_scratch_bytes(bool lsq, int limbs, int m, int n) {
 
 int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_a,
                const double* d_b, double* d_q, double* d_r, double* d_x, double* d_z,
-               xqr_status* d_st, size_t scratch_off, bool timed) {
+               xqr_status* d_st, size_t scratch_off, bool timed, int64_t sys = 0) {
     const int ncol = n + (lsq ? 1 : 0);
     xb::GridParams p{};
+    p.sys = sys;
     p.m = m;
     p.n = n;
     if (limbs <= 2) {
@@ -237,6 +236,19 @@ int solve_device(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t m, in
     if (batch == 1 && use_grid_path(ctx, limbs, (int)m, (int)n))
         return solve_grid(ctx, lsq, limbs, (int)m, (int)n, d_a, d_b, d_q, d_r, d_x, d_z, d_st,
                           scratch_off, timed);
+    if (m > 32 * xb::kMaxRowsPerLane) {
+        // taller than one CTA holds: system by system on the grid kernels
+        const size_t L2 = 2 * (size_t)limbs;
+        for (int64_t s = 0; s < batch; ++s) {
+            const int rc = solve_grid(
+                ctx, lsq, limbs, (int)m, (int)n, d_a + s * m * n * L2, lsq ? d_b + s * m * L2 : nullptr,
+                lsq ? nullptr : d_q + s * m * n * L2, lsq ? nullptr : d_r + s * n * n * L2,
+                lsq ? d_x + s * n * L2 : nullptr, lsq ? d_z + s * limbs : nullptr, d_st + s, scratch_off,
+                timed && s == 0, s);
+            if (rc) return rc;
+        }
+        return 0;
+    }
     xb::SolveParams p{};
     p.batch = batch;
     p.m = (int)m;
@@ -566,6 +578,22 @@ static int solve_host(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t 
     }
     if (batch == 0) return 0;
     cudaSetDevice(ctx->device);
+    if (batch > 1 && m > 32 * xb::kMaxRowsPerLane) {
+        // taller than one CTA holds: system by system on the grid kernels
+        const size_t L2 = 2 * (size_t)limbs;
+        int first = 0;
+        for (int64_t s = 0; s < batch; ++s) {
+            xqr_status one{};
+            const int rc = solve_host(ctx, lsq, limbs, 1, m, n, a + s * m * n * L2, lsq ? b + s * m * L2 : nullptr,
+                                      lsq ? nullptr : q + s * m * n * L2, lsq ? nullptr : r + s * n * n * L2,
+                                      lsq ? x + s * n * L2 : nullptr, lsq ? z + s * limbs : nullptr, &one);
+            if (rc >= XQR_DIMENSION) return rc;  // a call-level failure
+            one.system = s;
+            if (st) st[s] = one;
+            if (rc && !first) first = rc;
+        }
+        return first;
+    }
     if (batch > 1) return solve_host_batched(ctx, lsq, limbs, batch, m, n, a, b, q, r, x, z, st);
     const size_t L2 = 2 * (size_t)limbs;
     const size_t a_b = sizeof(double) * batch * m * n * L2;

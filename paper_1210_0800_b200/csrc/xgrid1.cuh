@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
         if (tid == 0) {
             unsigned long long key = s_key;
             xqr_status st;
-            st.system = 0;
+            st.system = p.sys;
             st.code = key == kNoError ? 0 : (int)(key & 15);
             st.column = key == kNoError ? 0 : (int)((key >> 4) & 0xFFFFF);
             *p.st = st;

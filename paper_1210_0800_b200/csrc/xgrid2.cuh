@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
         const unsigned long long key = __ldcg(p.key);
         if (p.trace) p.trace[n * 8 + 4] = g2_timer();
         xqr_status st;
-        st.system = 0;
+        st.system = p.sys;
         st.code = key == kNoError ? 0 : (int)(key & 15);
         st.column = key == kNoError ? 0 : (int)((key >> 4) & 0xFFFFF);
         *p.st = st;
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(kG2BsThreads, 1) grid2_backsub_kernel(GridPara
     if (p.trace && threadIdx.x == 0) p.trace[n * 8 + 6] = g2_timer();
     if (threadIdx.x == 0 && s_key != kNoError) {
         xqr_status st;
-        st.system = 0;
+        st.system = p.sys;
         st.code = (int)(s_key & 15);
         st.column = (int)((s_key >> 4) & 0xFFFFF);
         *p.st = st;

@@ -88,6 +88,7 @@ struct GridParams {
     int cs;                     // CTAs per cluster
     int* counters;              // [0] pre-pass arrivals, [1] final arrivals, [2] abort word
     int pair_bulk;              // xgrid2: update trailing columns two at a time (lockstep)
+    int64_t sys;                // index written into the status (a batch solved system by system)
 };
 
 // single systems (the grid kernels) take m <= kGridMaxRows; batches (one CTA

@@ -556,8 +556,8 @@ def test_dimension_errors_device(port, L, m, n):
 def test_tall_single_systems(port, L, m):
     """m in (1024, 2048]: qd on 8-CTA clusters with 4 rows per lane pair, dd / d
     on the CTA-per-column kernel with 8 rows per thread; bitwise, plus the
-    device metrics.  Batches of such systems are refused (one CTA per system
-    holds at most 1024 rows)."""
+    device metrics.  Batches of such systems run system by system on the grid
+    kernels (one CTA per system holds at most 1024 rows) with the same bits."""
     for n in (3, 9):
         a, b = port.gen_system(L, m, n, 1.0, 9100 + m + n)
         q, r, _ = port.mgs_qr(a)
@@ -570,5 +570,44 @@ def test_tall_single_systems(port, L, m):
         assert_same(gz, z, f"z m={m} n={n}")
         assert_same(xqr.residual_max_entry(a, q, r), port.residual_max_entry(a, q, r)[0], "residual")
         assert_same(xqr.orthogonality_defect(q), port.orthogonality_defect(q)[0], "orthogonality")
-    with pytest.raises(xqr.usage_error):
-        xqr.lsq_solve_batched(a[None].repeat(2, 0), b[None].repeat(2, 0))
+    a2, b2 = port.gen_system(L, m, n, 1.0, 9200 + m)
+    A = np.stack([a, a2])
+    B = np.stack([b, b2])
+    bx, bz, codes, _ = xqr.lsq_solve_batched(A, B)
+    assert not codes.any()
+    assert_same(bx[0], x, "batched x[0]")
+    assert_same(bx[1], port.lsq_solve(a2, b2)[0], "batched x[1]")
+    bq, br, codes, _ = xqr.mgs_qr_batched(A)
+    assert not codes.any()
+    assert_same(bq[0], q, "batched q[0]")
+    assert_same(br[1], port.mgs_qr(a2)[1], "batched r[1]")
+
+
+def test_tall_batch_device_api(port):
+    """The device-pointer batched call with m > 1024: system by system on the
+    grid kernels, statuses carry their system index."""
+    torch = pytest.importorskip("torch")
+    L, m, n = 4, 1100, 5
+    sys_ab = [port.gen_system(L, m, n, 1.0, 9300 + s) for s in range(3)]
+    A = np.stack([ab[0] for ab in sys_ab])
+    A[1, 2] = A[1, 0]  # system 1 breaks down at column 3
+    B = np.stack([ab[1] for ab in sys_ab])
+    ctx = xqr.context(0)
+    da, db = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    dx = torch.zeros((3, n, 2, L), dtype=torch.float64, device="cuda")
+    dz = torch.zeros((3, L), dtype=torch.float64, device="cuda")
+    dst = torch.zeros((3, 2), dtype=torch.int64, device="cuda")
+    try:
+        ctx.lsq_solve_batched_device(L, 3, m, n, da.data_ptr(), db.data_ptr(), dx.data_ptr(),
+                                     dz.data_ptr(), dst.data_ptr())
+    except xqr.breakdown_error:
+        pass  # the call reports the first failing system; statuses are per system
+    torch.cuda.synchronize()
+    st = dst.cpu().numpy()
+    code = st[:, 0] & 0xFFFFFFFF
+    col = st[:, 0] >> 32
+    assert list(code) == [0, 1, 0] and col[1] == 3 and list(st[:, 1]) == [0, 1, 2]
+    for s in (0, 2):
+        x, z, _ = port.lsq_solve(A[s], B[s])
+        assert_same(dx[s].cpu().numpy(), x, f"x[{s}]")
+        assert_same(dz[s].cpu().numpy(), z, f"z[{s}]")
