@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
     // in program order is recorded (an overflow in a bulk update is only
     // recorded: the column's own normalisation fails later)
     constexpr int kFlagErr = 0x10000;
-    if (p.trace && blockIdx.x == 0 && g.tid == 0) p.trace[n * 8 + 6] = g2_timer();
+    if (p.trace && blockIdx.x == 0 && g.tid == 0) p.trace[n * 8 + 2] = g2_timer();  // pre-pass done
 
     // normalise column j (owner cluster) and publish it.  Returns false on error.
     auto normalize_publish = [&](int j) -> bool {

@@ -36,6 +36,9 @@ def main():
         last = t[-1]
         start, grid_end, bs_start, bs_end = int(last[8]), int(last[5]), int(last[6]), int(last[7])
         fact = (grid_end - start) / 1e3 if start else float("nan")
+        pre_end = int(last[3]) if args.limbs == 4 else 0  # xgrid2: norm pre-pass done (row n, slot 2)
+        if pre_end and start:
+            print(f"  pre-pass (column norms + threshold) {(pre_end - start) / 1e3:.1f} us")
         if args.pivots and args.limbs <= 2:
             # xgrid1 stamps: 0 q_{j-1} in hand, 1 column j updated, 2 published
             T = t[:, 1:9].astype(np.int64)
