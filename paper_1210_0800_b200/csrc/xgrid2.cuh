@@ -10,20 +10,25 @@
 //   * a LANE PAIR owns a row: the even lane computes the real part, the odd
 //     lane the imaginary part of every complex quantity (the two halves of a
 //     complex multiply / add / divide are independent -- complex.hpp:26-65);
-//   * a column belongs to a thread-block CLUSTER of CS CTAs (CS = 4 for
-//     m = 256 and 512): 4 warps per CTA, 16 lane pairs per warp; two CTAs
-//     (of different clusters) share an SM, so one cluster's latency-bound
-//     chains fill the other's issue gaps;
+//   * a column belongs to a thread-block CLUSTER of CS CTAs (grid_shape:
+//     up to 4 for m <= 256, 8 for 256 < m <= 512 and m > 1024): 4 warps per
+//     CTA, 16 lane pairs per warp; two CTAs (of different clusters) share an
+//     SM, so one cluster's latency-bound chains fill the other's issue gaps;
 //   * the fixed reduction tree (reduction.hpp:34-40) runs in-lane (rows of a
 //     pair), then over lane pairs by shuffles, then over the cluster's warp
-//     partials read through distributed shared memory -- the same pairing as
-//     the sequential tree_reduce, since rows are laid out consecutively;
-//   * every warp computes the pivot's sqrt / reciprocal redundantly (no
-//     broadcast hop), then each lane divides its own half of its row.
+//     partials, staged into local shared memory with one DSMEM load per
+//     thread -- the same pairing as the sequential tree_reduce, since rows
+//     are laid out consecutively;
+//   * warp 0 of each CTA computes the pivot's sqrt / reciprocal (call-form
+//     qd ops: one hot copy in the instruction cache) and shares them through
+//     shared memory, then each lane divides its own half of its row;
+//   * for 256 < m <= 512 the trailing (off-chain) columns are updated two at
+//     a time in lockstep (addc2, g2_tree2).
 // Columns are distributed cyclically over clusters (column j -> cluster
 // j mod G); q_k is the finished column itself in the (AoS) workspace,
-// published with a release counter and acquired by every other cluster; the
-// owner of column k+1 updates and normalises it first (look-ahead).  The
+// published with a release counter (carrying a failure bit) and acquired by
+// every other cluster; the owner of column k+1 updates and normalises it
+// first (look-ahead).  The
 // working copy uses the reference's own memory image (column-major, row =
 // re limbs then im limbs), so the loads of a lane pair are contiguous.
 #pragma once
