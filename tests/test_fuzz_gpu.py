@@ -39,10 +39,13 @@ def test_fuzz_single_systems(port):
     cases = int(os.environ.get("XQR_FUZZ_CASES", "48"))
     for c in range(cases):
         L = int(rng.choice([1, 2, 4]))
-        m = int(rng.choice([2, 7, 16, 31, 33, 64, 65, 100, 129, 200, 256, 257, 300]))
-        if L == 4:
+        sizes = [2, 7, 16, 31, 33, 64, 65, 100, 129, 200, 256, 257, 300]
+        if os.environ.get("XQR_FUZZ_BIG") == "1":  # tall systems too (slower oracle)
+            sizes += [400, 511, 512, 700, 1024, 1100, 2048]
+        m = int(rng.choice(sizes))
+        if L == 4 and os.environ.get("XQR_FUZZ_BIG") != "1":
             m = min(m, 257)
-        n = int(rng.integers(1, min(m, 64 if L == 4 else 96) + 1))
+        n = int(rng.integers(1, min(m, 64 if L == 4 else 96, 24 if m > 512 else 96) + 1))
         g = float(rng.choice([1.0, 1.0, 4.0, 8.0, 16.0]))
         a, b = port.gen_system(L, m, n, g, int(rng.integers(1, 1 << 30)))
         if rng.random() < 0.15 and n > 2:  # a dependent column somewhere
