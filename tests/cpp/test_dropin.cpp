@@ -142,6 +142,14 @@ int main() {
     random_parity<double_double>(32, 32, 1);
     random_parity<double_double>(45, 20, 9);
     random_parity<quad_double>(24, 24, 3);
+    // the single-system grid kernels through the same C++ API: double-double
+    // CTA-per-column grid, quad-double clusters (4 CTAs; 8 CTAs with paired
+    // bulk updates), and a system taller than one CTA holds (batched: system
+    // by system)
+    random_parity<double_double>(256, 64, 11);
+    random_parity<quad_double>(256, 40, 12);
+    random_parity<quad_double>(300, 45, 13);
+    random_parity<quad_double>(1100, 5, 14);
     std::printf("%s %d checks, %d failures\n", failures ? "FAIL" : "PASS", checks, failures);
     return failures ? 1 : 0;
 }
