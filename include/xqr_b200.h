@@ -132,6 +132,11 @@ int xqr_orthogonality_defect_batched_device(xqr_ctx* ctx, int limbs, int64_t bat
  * b may be NULL.  Bitwise identical to the reference's draws. */
 int xqr_gen_systems(int limbs, int64_t batch, int64_t m, int64_t n, double g, uint64_t seed,
                     int64_t first_stream, int threads, double* a, double* b);
+/* Same, with the modulus distribution of random.hpp:44-71 (`--modulus-dist`,
+ * xqr_main.cpp:209-213): dist 0 = log_uniform (the default above), 1 =
+ * linear_uniform (modulus uniform on [10^-g, 10^g]). */
+int xqr_gen_systems_dist(int limbs, int64_t batch, int64_t m, int64_t n, double g, int dist,
+                         uint64_t seed, int64_t first_stream, int threads, double* a, double* b);
 
 /* ---- test / instrumentation --------------------------------------------- */
 /* Elementwise device arithmetic, op codes as oracle/xqr_oracle.h xo_arith:
@@ -142,6 +147,10 @@ int xqr_arith(xqr_ctx* ctx, int limbs, int op, int64_t count, const double* a, c
 /* Number of kernel launches this ctx has issued (for the bench's
  * gpu_launches claim). */
 int64_t xqr_ctx_launch_count(xqr_ctx* ctx);
+/* Number of single-system solves this ctx re-routed from the persistent grid
+ * kernels to the one-CTA kernel because the grid could not be made
+ * co-resident (same results bit for bit; m <= 1024 only). */
+int64_t xqr_ctx_grid_fallbacks(xqr_ctx* ctx);
 /* Accumulated device time (ms) of the most recent solver launch, measured
  * with CUDA events on the ctx stream (0 if not yet available). */
 float xqr_ctx_last_kernel_ms(xqr_ctx* ctx);

@@ -92,6 +92,8 @@ class Oracle:
             self._plsq.argtypes = [ci, _i64, _i64, _dp, _dp, _dp, _dp, ci, sp]
             self._pmgs = L.ref_par_mgs_qr
             self._pmgs.argtypes = [ci, _i64, _i64, _dp, _dp, _dp, ci, ci, sp]
+            self._acc = L.ref_accuracy_csv
+            self._acc.argtypes = [ci, _i64, _i64, _dp, ci, _i64, ctypes.c_uint64, ci, ctypes.c_char_p, _i64]
             self._batch = L.ref_lsq_solve_batch
             self._batch.argtypes = [ci, _i64, _i64, _i64, _dp, _dp, _dp, _dp, ci,
                                     ctypes.POINTER(ctypes.c_int32)]
@@ -154,6 +156,13 @@ class Oracle:
         self._batch(L, batch, m, n, _ptr(np.ascontiguousarray(a)), _ptr(np.ascontiguousarray(b)),
                     _ptr(x), _ptr(z), threads, codes.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
         return x, z, codes
+
+    def accuracy_csv(self, limbs, m, n, g_values, trials, seed=1, linear=False):
+        """The reference's run_accuracy_sweep + accuracy_csv text (reference build only)."""
+        g = np.ascontiguousarray(g_values, dtype=np.float64)
+        buf = ctypes.create_string_buffer(1 << 16)
+        rc = self._acc(limbs, m, n, _ptr(g), len(g), trials, seed, int(linear), buf, len(buf))
+        return buf.value.decode(), rc
 
     def back_substitute(self, r, y):
         rc_, rn, _, L = r.shape

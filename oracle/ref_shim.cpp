@@ -8,7 +8,9 @@
 // baseline in bench.py.  Nothing here is product code; the built library
 // lives in oracle/_ref/ (git-ignored, not gpurun-ignored).
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
+#include <string>
 #include <thread>
 #include <type_traits>
 #include <vector>
@@ -260,6 +262,31 @@ int ref_lsq_solve_batch(int limbs, int64_t batch, int64_t m, int64_t n, const do
     }
     for (auto& th : pool) th.join();
     return 0;
+}
+
+// The reference's own accuracy sweep and CSV (run_accuracy_sweep,
+// experiment.hpp:157-176; accuracy_csv, :412-433), for the CLI parity test.
+// Writes at most `cap` bytes (NUL-terminated) into out; returns the code of
+// an exception that escaped the sweep (0 = ok).
+int ref_accuracy_csv(int limbs, int64_t m, int64_t n, const double* g, int ng, int64_t trials,
+                     uint64_t seed, int linear, char* out, int64_t cap) {
+    accuracy_config cfg;
+    cfg.precision = limbs == 1 ? precision_tag::d : (limbs == 2 ? precision_tag::dd : precision_tag::qd);
+    cfg.m = (std::size_t)m;
+    cfg.n = (std::size_t)n;
+    cfg.g_values.assign(g, g + ng);
+    cfg.trials = (std::size_t)trials;
+    cfg.seed = seed;
+    cfg.dist = linear ? modulus_dist::linear_uniform : modulus_dist::log_uniform;
+    std::string text;
+    xo_status st{};
+    int rc = guarded(&st, [&] { text = accuracy_csv(run_accuracy_sweep(cfg)); });
+    if (cap > 0) {
+        const size_t k = std::min(text.size(), (size_t)(cap - 1));
+        std::memcpy(out, text.data(), k);
+        out[k] = 0;
+    }
+    return rc;
 }
 
 }  // extern "C"

@@ -156,7 +156,10 @@ _SIGNATURES = {
     "xqr_orthogonality_defect_batched_device": ([_vp, _ci, _i64, _i64, _i64, _vp, _vp, _vp], _ci),
     "xqr_gen_systems": ([_ci, _i64, _i64, _i64, ctypes.c_double, ctypes.c_uint64, _i64, _ci, _dp,
                          _dp], _ci),
+    "xqr_gen_systems_dist": ([_ci, _i64, _i64, _i64, ctypes.c_double, _ci, ctypes.c_uint64, _i64, _ci,
+                              _dp, _dp], _ci),
     "xqr_ctx_launch_count": ([_vp], _i64),
+    "xqr_ctx_grid_fallbacks": ([_vp], _i64),
     "xqr_ctx_last_kernel_ms": ([_vp], ctypes.c_float),
 }
 
@@ -221,6 +224,11 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(self._lib.xqr_ctx_launch_count(self.handle))
+
+    @property
+    def grid_fallbacks(self) -> int:
+        """Single systems re-routed to the one-CTA kernel (grid not placeable)."""
+        return int(self._lib.xqr_ctx_grid_fallbacks(self.handle))
 
     @property
     def last_kernel_ms(self) -> float:
@@ -447,48 +455,76 @@ def mgs_qr_batched(a, device: int = 0, raise_first: bool = False):
     return q, r, codes, cols
 
 
+MODULUS_DIST = {"log": 0, "linear": 1}  # random.hpp:44 modulus_dist
+
+
 def gen_systems(limbs: int, batch: int, m: int, n: int, g: float = 1.0, seed: int = 1,
-                first_stream: int = 0, threads: int | None = None, rhs: bool = True):
+                first_stream: int = 0, threads: int | None = None, rhs: bool = True,
+                dist: str = "log"):
     """The reference generator (experiment.hpp:64-79) on the host: returns
     a (batch, n, m, 2, L) and b (batch, m, 2, L).  first_stream=-1 draws one
     system from split_mix64(seed) itself (the reference's single-system
-    experiments); otherwise system s uses split_mix64(seed).split(first_stream+s)."""
+    experiments); otherwise system s uses split_mix64(seed).split(first_stream+s).
+    dist: "log" (log-uniform modulus, the default) or "linear" (random.hpp:57-71)."""
     lib = load_library()
+    if dist not in MODULUS_DIST:
+        raise usage_error(f"unknown modulus distribution '{dist}'")
     a = np.zeros((batch, n, m, 2, limbs))
     b = np.zeros((batch, m, 2, limbs)) if rhs else None
     threads = threads or min(32, os.cpu_count() or 1)
-    rc = lib.xqr_gen_systems(limbs, batch, m, n, g, seed, first_stream, threads,
-                             a.ctypes.data_as(_dp), b.ctypes.data_as(_dp) if rhs else None)
+    rc = lib.xqr_gen_systems_dist(limbs, batch, m, n, g, MODULUS_DIST[dist], seed, first_stream, threads,
+                                  a.ctypes.data_as(_dp), b.ctypes.data_as(_dp) if rhs else None)
     if rc:
         _raise(rc, what="gen_systems")
     return (a, b) if rhs else a
 
 
 def accuracy_sweep(limbs: int, m: int = 32, n: int = 32, g_values=(1.0,), trials: int = 100,
-                   seed: int = 1, device: int = 0):
-    """The reference's accuracy sweep (experiment.hpp:117-176, paper Table 2)
-    on the device: for each g (index gi), `trials` matrices drawn from
-    split_mix64(seed).split(gi*trials + t) (log-uniform modulus in
-    [10^-g, 10^g]), mgs_qr of each (batched kernel), e = residual_max_entry
-    (device metric), log10(e's leading limb); breakdowns are excluded but
-    counted.  Returns one dict per g: g, trials, exclusions, m_e = min log10 e,
-    M_e = max log10 e, D_e = m_e - M_e, log10_e (per kept trial)."""
+                   seed: int = 1, device: int = 0, dist: str = "log"):
+    """The reference's accuracy sweep (run_accuracy_sweep, experiment.hpp:117-176,
+    paper Table 2) on the device: for each g (index gi), `trials` matrices
+    drawn from split_mix64(seed).split(gi*trials + t), mgs_qr of each (one
+    batched launch), e = residual_max_entry (device metric), log10(e's
+    leading limb).  As in the reference's trial loop, only breakdown_error
+    excludes a trial (counted in `exclusions`); any other error -- of the
+    factorisation or of the residual metric -- propagates, the first one in
+    trial order.  Returns one dict per g: g, trials (completed),
+    exclusions, m_e = min log10 e, M_e = max log10 e, D_e = m_e - M_e,
+    log10_e (per completed trial), wall_seconds (GPU generation excluded:
+    host generation + solve + metric)."""
+    import time
+
+    if trials < 1:
+        raise usage_error("trials must be at least 1")
+    if m < n or n < 1:
+        raise usage_error("need rows >= cols >= 1")
     out = []
     for gi, g in enumerate(g_values):
-        a = gen_systems(limbs, trials, m, n, float(g), seed, gi * trials, rhs=False)
-        q, r, codes, _ = mgs_qr_batched(a, device=device)
+        t0 = time.perf_counter()
+        a = gen_systems(limbs, trials, m, n, float(g), seed, gi * trials, rhs=False, dist=dist)
+        q, r, codes, cols = mgs_qr_batched(a, device=device)
         keep = codes == 0
-        e, ecodes = residual_max_entry_batched(a[keep], q[keep], r[keep], device=device) if keep.any() \
-            else (np.zeros((0, limbs)), np.zeros(0, dtype=np.int32))
-        log10_e = np.log10(e[:, 0]) if len(e) else np.zeros(0)
+        e = np.zeros((trials, limbs))
+        ecodes = np.zeros(trials, dtype=np.int32)
+        if keep.any():
+            e[keep], ecodes[keep] = residual_max_entry_batched(a[keep], q[keep], r[keep], device=device)
+        # the reference's loop raises at the first trial whose factorisation
+        # fails with anything but a breakdown, or whose metric fails
+        bad = ((codes != XQR_OK) & (codes != XQR_BREAKDOWN)) | (ecodes != XQR_OK)
+        if bad.any():
+            t = int(np.nonzero(bad)[0][0])
+            code = int(codes[t]) if codes[t] != XQR_OK else int(ecodes[t])
+            _raise(code, int(cols[t]), f"accuracy trial {t} (g={g})")
+        log10_e = np.log10(e[keep, 0])
         rec = {"g": float(g), "m": m, "n": n, "limbs": limbs, "trials": int(keep.sum()),
-               "exclusions": int((~keep).sum()), "log10_e": log10_e.tolist()}
+               "exclusions": int((codes == XQR_BREAKDOWN).sum()), "log10_e": log10_e.tolist()}
         if len(log10_e):
             rec["m_e"] = float(log10_e.min())
             rec["M_e"] = float(log10_e.max())
             rec["D_e"] = rec["m_e"] - rec["M_e"]
         else:
             rec["m_e"] = rec["M_e"] = rec["D_e"] = float("nan")
+        rec["wall_seconds"] = time.perf_counter() - t0
         out.append(rec)
     return out
 

@@ -5,7 +5,8 @@ accuracy subcommands, tools/xqr_main.cpp:121-196, :249-328):
                                                  [--workers N] [--normalize-mode M]
     python -m paper_1210_0800_b200.cli solve A.mat b.mat [--x-out P] [--precision cqd]
     python -m paper_1210_0800_b200.cli accuracy [--precision cdd] [--m 32] [--n 32]
-                                               [--g 1,4,8] [--trials 100] [--seed 1] [--out F]
+                                               [--g 1 4 8] [--trials 100] [--seed 1]
+                                               [--modulus-dist log|linear] [--paper-scale] [--out F]
 
 Files are the reference's matrix format (matrix_io.py); outputs are written
 atomically (temp + rename, xqr_main.cpp:42-58); stdout prints the same
@@ -131,30 +132,38 @@ def run_solve(o) -> None:
     print(f"residual_norm {shortest(z[0])}")
 
 
-def run_accuracy(o) -> None:
-    """accuracy sweep on the GPU; CSV as the reference's accuracy_csv
-    (experiment.hpp:415-433)."""
-    import time
+ACCURACY_CSV_HEADER = "kind,precision,m,n,g,trials,exclusions,m_e,M_e,D_e,wall_seconds"
 
+
+def accuracy_csv(precision: str, records) -> str:
+    """experiment.hpp:412-433 accuracy_csv: header, then one `accuracy,` row
+    per g in shortest round-trip decimal."""
+    lines = [ACCURACY_CSV_HEADER + "\n"]
+    for rec in records:
+        lines.append(f"accuracy,{precision},{rec['m']},{rec['n']},{shortest(rec['g'])},{rec['trials']},"
+                     f"{rec['exclusions']},{shortest(rec['m_e'])},{shortest(rec['M_e'])},"
+                     f"{shortest(rec['D_e'])},{shortest(rec['wall_seconds'])}\n")
+    return "".join(lines)
+
+
+def run_accuracy(o) -> None:
+    """accuracy sweep on the GPU (xqr_main.cpp:216-226 -> run_accuracy_sweep,
+    experiment.hpp:157-176): ONE sweep over every g, so g index gi draws the
+    streams split(gi*trials + t) exactly as the reference; CSV as the
+    reference's accuracy_csv."""
     import paper_1210_0800_b200 as xqr
 
     L = PRECISION_LIMBS.get(o.precision)
     if L is None:
         raise xqr.usage_error(f"unknown precision token '{o.precision}'")
-    if o.trials < 1:
-        raise xqr.usage_error("trials must be at least 1")
-    if o.m < o.n or o.n == 0:
-        raise xqr.usage_error("need rows >= cols >= 1")
-    gs = [float(t) for t in o.g.split(",")]
-    lines = ["precision,m,n,g,trials,exclusions,m_e,M_e,D_e,wall_seconds\n"]
-    for rec_g in gs:
-        t0 = time.perf_counter()
-        rec = xqr.accuracy_sweep(L, o.m, o.n, [rec_g], o.trials, o.seed)[0]
-        dt = time.perf_counter() - t0
-        lines.append(f"{o.precision},{o.m},{o.n},{shortest(rec['g'])},{rec['trials']},"
-                     f"{rec['exclusions']},{shortest(rec['m_e'])},{shortest(rec['M_e'])},"
-                     f"{shortest(rec['D_e'])},{shortest(dt)}\n")
-    text = "".join(lines)
+    if o.modulus_dist not in xqr.MODULUS_DIST:
+        raise xqr.usage_error(f"unknown modulus distribution '{o.modulus_dist}'")
+    trials = o.trials * 10 if o.paper_scale else o.trials
+    # --g is repeatable and takes several values (CLI11 vector option); a
+    # comma-separated list is accepted too
+    gs = [float(t) for tok in (o.g or ["1"]) for t in str(tok).split(",") if t]
+    records = xqr.accuracy_sweep(L, o.m, o.n, gs, trials, o.seed, dist=o.modulus_dist)
+    text = accuracy_csv(o.precision, records)
     if o.out:
         write_file_atomic(o.out, text)
     else:
@@ -180,12 +189,14 @@ def main(argv=None) -> int:
     s.add_argument("--x-out", default="")
     s.add_argument("--workers", type=int, default=int(os.environ.get("XQR_WORKERS", "1")))
     a = sub.add_parser("accuracy")
-    a.add_argument("--precision", default="cd")
+    a.add_argument("--precision", required=True)
     a.add_argument("--m", type=int, default=32)
     a.add_argument("--n", type=int, default=32)
-    a.add_argument("--g", default="1")
+    a.add_argument("--g", action="extend", nargs="+", default=None)
     a.add_argument("--trials", type=int, default=100)
     a.add_argument("--seed", type=int, default=1)
+    a.add_argument("--modulus-dist", default="log")
+    a.add_argument("--paper-scale", action="store_true")
     a.add_argument("--out", default="")
     try:
         o = ap.parse_args(argv)

@@ -32,6 +32,7 @@ struct xqr_ctx {
     void* pinned_out = nullptr;
     size_t pinned_out_bytes = 0;
     int64_t launches = 0;
+    int64_t grid_fallbacks = 0;  // single systems re-routed to the CTA kernel
     int num_sms = 148;
     bool coop = false;
     std::string last_error;
@@ -148,6 +149,17 @@ size_t grid_scratch_bytes(bool lsq, int limbs, int m, int n) {
            8 * 256;
 }
 
+// solve_grid's answer when the persistent grid cannot be placed (the
+// cooperative / cluster launch finds no co-residency: an MPS partition, a
+// smaller part); the caller re-routes the system to the CTA kernel, which
+// computes the same bits.
+constexpr int kGridUnplaceable = -1;
+
+bool unplaceable(cudaError_t e) {
+    return e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorInvalidConfiguration ||
+           e == cudaErrorInvalidClusterSize;
+}
+
 int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_a,
                const double* d_b, double* d_q, double* d_r, double* d_x, double* d_z,
                xqr_status* d_st, size_t scratch_off, bool timed, int64_t sys = 0) {
@@ -197,15 +209,25 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     if (p.trace) cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * 16 * (size_t)(n + 1), ctx->stream);
     int per_sm = limbs == 4 ? xb::kGrid2PerSM : 1;
     if (const char* e = std::getenv("XQR_GRID_PER_SM")) per_sm = std::max(1, std::atoi(e));  // dev
-    const int max_clusters = per_sm * ctx->num_sms / p.cs;
+    // SMs the persistent grid may occupy; XQR_GRID_MAX_SMS emulates a
+    // partitioned device (MPS) for the re-routing test
+    int sms = ctx->num_sms;
+    if (const char* e = std::getenv("XQR_GRID_MAX_SMS")) sms = std::max(0, std::min(sms, std::atoi(e)));
+    const int max_clusters = per_sm * sms / p.cs;
+    const int grid1 = std::min(ncol, sms);
+    if ((limbs <= 2 && grid1 < 1) || (limbs == 4 && max_clusters < 1)) return kGridUnplaceable;
     if (timed) cudaEventRecord(ctx->ev0, ctx->stream);
     switch (limbs) {
-        case 1: e = xb::launch_grid_L1(p, std::min(ncol, ctx->num_sms), lsq, ctx->stream); break;
-        case 2: e = xb::launch_grid_L2(p, std::min(ncol, ctx->num_sms), lsq, ctx->stream); break;
+        case 1: e = xb::launch_grid_L1(p, grid1, lsq, ctx->stream); break;
+        case 2: e = xb::launch_grid_L2(p, grid1, lsq, ctx->stream); break;
         default: e = xb::launch_grid_L4(p, max_clusters, lsq, ctx->stream); break;
     }
     if (timed) cudaEventRecord(ctx->ev1, ctx->stream);
     ctx->timed = timed;
+    if (e != cudaSuccess && unplaceable(e)) {
+        cudaGetLastError();  // not sticky: clear it and let the caller re-route
+        return kGridUnplaceable;
+    }
     ctx->launches += 1;
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "grid kernel launch");
     if (p.trace) {
@@ -233,9 +255,18 @@ int solve_device(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t m, in
                  const double* d_a, const double* d_b, double* d_q, double* d_r, double* d_x,
                  double* d_z, xqr_status* d_st, size_t scratch_off, bool timed) {
     const int ncol = (int)n + (lsq ? 1 : 0);
-    if (batch == 1 && use_grid_path(ctx, limbs, (int)m, (int)n))
-        return solve_grid(ctx, lsq, limbs, (int)m, (int)n, d_a, d_b, d_q, d_r, d_x, d_z, d_st,
-                          scratch_off, timed);
+    if (batch == 1 && use_grid_path(ctx, limbs, (int)m, (int)n)) {
+        const int rc = solve_grid(ctx, lsq, limbs, (int)m, (int)n, d_a, d_b, d_q, d_r, d_x, d_z, d_st,
+                                  scratch_off, timed);
+        if (rc != kGridUnplaceable) return rc;
+        if (m > 32 * xb::kMaxRowsPerLane) {
+            ctx->last_error = "grid kernel cannot be placed on this device (m > 1024 has no CTA kernel)";
+            return XQR_CUDA;
+        }
+        // the grid cannot be made co-resident here: the CTA kernel computes
+        // the same bits on one SM
+        ctx->grid_fallbacks += 1;
+    }
     if (m > 32 * xb::kMaxRowsPerLane) {
         // taller than one CTA holds: system by system on the grid kernels
         const size_t L2 = 2 * (size_t)limbs;
@@ -245,6 +276,10 @@ int solve_device(xqr_ctx* ctx, bool lsq, int limbs, int64_t batch, int64_t m, in
                 lsq ? nullptr : d_q + s * m * n * L2, lsq ? nullptr : d_r + s * n * n * L2,
                 lsq ? d_x + s * n * L2 : nullptr, lsq ? d_z + s * limbs : nullptr, d_st + s, scratch_off,
                 timed && s == 0, s);
+            if (rc == kGridUnplaceable) {
+                ctx->last_error = "grid kernel cannot be placed on this device (m > 1024 has no CTA kernel)";
+                return XQR_CUDA;
+            }
             if (rc) return rc;
         }
         return 0;
@@ -350,6 +385,8 @@ int xqr_ctx_synchronize(xqr_ctx* ctx) {
 const char* xqr_ctx_last_error(xqr_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "no ctx"; }
 
 int64_t xqr_ctx_launch_count(xqr_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int64_t xqr_ctx_grid_fallbacks(xqr_ctx* ctx) { return ctx ? ctx->grid_fallbacks : 0; }
 
 float xqr_ctx_last_kernel_ms(xqr_ctx* ctx) {
     if (!ctx || !ctx->timed) return 0.f;
@@ -699,21 +736,40 @@ int xqr_back_substitute(xqr_ctx* ctx, int limbs, int64_t rows, int64_t cols, con
 
 // ---- verification metrics (mgs.hpp:161-178, :208-222) -------------------------------
 namespace {
-int metric_device(xqr_ctx* ctx, int which, int limbs, int64_t batch, int64_t m, int64_t n,
+// Scratch of one metric launch (partials + per-system flags), laid out in an
+// arena plan that already holds any I/O regions of the call: the arena is
+// sized ONCE, before the caller takes device pointers into it.
+struct metric_scratch {
+    size_t o_part, o_flg;
+};
+metric_scratch plan_metric(arena_plan& plan, int which, int limbs, int64_t batch, int64_t m, int64_t n) {
+    metric_scratch ms;
+    ms.o_part = plan.add(sizeof(double) * batch * xb::metric_blocks(which, (int)m, (int)n) * limbs);
+    ms.o_flg = plan.add(sizeof(int) * batch);
+    return ms;
+}
+
+int metric_launch(xqr_ctx* ctx, int which, int limbs, int64_t batch, int64_t m, int64_t n,
                   const double* d_a, const double* d_q, const double* d_r, double* d_out,
-                  xqr_status* d_st, size_t scratch_off) {
-    arena_plan plan;
-    const size_t o_part = plan.add(sizeof(double) * batch * xb::metric_blocks(which, (int)m, (int)n) * limbs);
-    const size_t o_flg = plan.add(sizeof(int) * batch);
-    cudaError_t e = ensure_arena(ctx, scratch_off + plan.total + 256);
-    if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
-    int* flags = reinterpret_cast<int*>(at(ctx, scratch_off + o_flg));
+                  xqr_status* d_st, const metric_scratch& ms) {
+    int* flags = reinterpret_cast<int*>(at(ctx, ms.o_flg));
     cudaMemsetAsync(flags, 0, sizeof(int) * batch, ctx->stream);
-    e = xb::launch_metric(limbs, which, batch, (int)m, (int)n, d_a, d_q, d_r, d_out,
-                          reinterpret_cast<double*>(at(ctx, scratch_off + o_part)), flags, d_st, ctx->stream);
+    cudaError_t e = xb::launch_metric(limbs, which, batch, (int)m, (int)n, d_a, d_q, d_r, d_out,
+                                      reinterpret_cast<double*>(at(ctx, ms.o_part)), flags, d_st, ctx->stream);
     ctx->launches += 2;
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "metric launch");
     return 0;
+}
+
+// device-pointer form: the arena holds only the metric scratch
+int metric_device(xqr_ctx* ctx, int which, int limbs, int64_t batch, int64_t m, int64_t n,
+                  const double* d_a, const double* d_q, const double* d_r, double* d_out,
+                  xqr_status* d_st) {
+    arena_plan plan;
+    const metric_scratch ms = plan_metric(plan, which, limbs, batch, m, n);
+    cudaError_t e = ensure_arena(ctx, plan.total + 256);
+    if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
+    return metric_launch(ctx, which, limbs, batch, m, n, d_a, d_q, d_r, d_out, d_st, ms);
 }
 
 int metric_host(xqr_ctx* ctx, int which, int limbs, int64_t batch, int64_t m, int64_t n, const double* a,
@@ -729,14 +785,18 @@ int metric_host(xqr_ctx* ctx, int which, int limbs, int64_t batch, int64_t m, in
     arena_plan plan;
     const size_t o_a = plan.add(a_b), o_q = plan.add(q_b), o_r = plan.add(r_b),
                  o_o = plan.add(sizeof(double) * batch * limbs), o_s = plan.add(sizeof(xqr_status) * batch);
+    // the metric's own scratch goes into the same plan: one allocation, made
+    // before any pointer into the arena is taken (a later growth would free
+    // the regions the copies below fill)
+    const metric_scratch ms = plan_metric(plan, which, limbs, batch, m, n);
     cudaError_t e = ensure_arena(ctx, plan.total + 256);
     if (e != cudaSuccess) return set_cuda_error(ctx, e, "workspace allocation");
     if (a_b) cudaMemcpyAsync(at(ctx, o_a), a, a_b, cudaMemcpyHostToDevice, ctx->stream);
     cudaMemcpyAsync(at(ctx, o_q), q, q_b, cudaMemcpyHostToDevice, ctx->stream);
     if (r_b) cudaMemcpyAsync(at(ctx, o_r), r, r_b, cudaMemcpyHostToDevice, ctx->stream);
-    int rc = metric_device(ctx, which, limbs, batch, m, n, (const double*)at(ctx, o_a),
+    int rc = metric_launch(ctx, which, limbs, batch, m, n, (const double*)at(ctx, o_a),
                            (const double*)at(ctx, o_q), (const double*)at(ctx, o_r), (double*)at(ctx, o_o),
-                           (xqr_status*)at(ctx, o_s), plan.total);
+                           (xqr_status*)at(ctx, o_s), ms);
     if (rc) return rc;
     std::vector<xqr_status> hst(batch);
     cudaMemcpyAsync(out, at(ctx, o_o), sizeof(double) * batch * limbs, cudaMemcpyDeviceToHost, ctx->stream);
@@ -771,14 +831,14 @@ int xqr_residual_max_entry_batched_device(xqr_ctx* ctx, int limbs, int64_t batch
     if (!ctx) return XQR_USAGE;
     if (int c = check_shape(ctx, nullptr, limbs, batch, m, n)) return c;
     cudaSetDevice(ctx->device);
-    return batch ? metric_device(ctx, 0, limbs, batch, m, n, d_a, d_q, d_r, d_out, d_st, 0) : 0;
+    return batch ? metric_device(ctx, 0, limbs, batch, m, n, d_a, d_q, d_r, d_out, d_st) : 0;
 }
 int xqr_orthogonality_defect_batched_device(xqr_ctx* ctx, int limbs, int64_t batch, int64_t m, int64_t n,
                                             const double* d_q, double* d_out, xqr_status* d_st) {
     if (!ctx) return XQR_USAGE;
     if (int c = check_shape(ctx, nullptr, limbs, batch, m, n)) return c;
     cudaSetDevice(ctx->device);
-    return batch ? metric_device(ctx, 1, limbs, batch, m, n, nullptr, d_q, nullptr, d_out, d_st, 0) : 0;
+    return batch ? metric_device(ctx, 1, limbs, batch, m, n, nullptr, d_q, nullptr, d_out, d_st) : 0;
 }
 
 int xqr_arith(xqr_ctx* ctx, int limbs, int op, int64_t count, const double* a, const double* b,

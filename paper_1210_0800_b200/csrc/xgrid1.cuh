@@ -161,13 +161,20 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
     for (int j = c; j < ncol; j += G) {
         R s = col_sq(colp(j));
         R nrm = rsqrt_ref(s);
-        if (!vfinite(s) || !vfinite(nrm)) {
-            if (tid == 0) record(0, 0, XQR_OVERFLOW);
+        const bool bad = !vfinite(s) || !vfinite(nrm);
+        if (tid == 0) {
+            if (bad) record(0, 0, XQR_OVERFLOW);
+            store_real<L>(p.norms + (int64_t)j * L, 1, nrm);
+            // the failure also travels in the norm itself (a NaN head), so
+            // every CTA derives the same pre-pass verdict from data fixed
+            // before the grid barrier (p.key keeps changing after it)
+            if (bad) p.norms[(int64_t)j * L] = __longlong_as_double(0x7ff8000000000000ll);
         }
-        if (tid == 0) store_real<L>(p.norms + (int64_t)j * L, 1, nrm);
     }
     cg::this_grid().sync();
-    // every CTA computes the same max (order-independent) and threshold
+    // every CTA computes the same max (order-independent), threshold and
+    // pre-pass verdict
+    bool pre_bad = false;
     {
         R best = rmake<R>(0.0);
         for (int j = tid; j < ncol; j += kGridThreads) {
@@ -177,6 +184,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
 #pragma unroll
             for (int l = 0; l < L; ++l) t[l] = __ldcg(q + l);
             load_real<L>(t, 1, v);
+            if (L > 1 && t[0] != t[0]) pre_bad = true;  // (double is unchecked)
             if (lt(best, v)) best = v;
         }
         // CTA max (exact: the max is order-independent)
@@ -197,7 +205,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
         __syncthreads();
     }
     const R thr = s_thr;
-    const bool pre_err = __ldcg(p.key) != kNoError;  // uniform: written before the grid sync
+    const bool pre_err = __syncthreads_or(pre_bad) != 0;  // grid-uniform: read from the norms
 
     // normalise column j (owner) and publish it; returns false on error
     auto normalize_publish = [&](int j) -> bool {

@@ -307,8 +307,13 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
         R s = col_norm2(g.col(j));
         R nrm = rsqrt_ref(s);
         if (g.crank == 0 && g.tid == 0) {
-            if (!vfinite(s) || !vfinite(nrm)) record(0, 0, XQR_OVERFLOW);
+            const bool bad = !vfinite(s) || !vfinite(nrm);
+            if (bad) record(0, 0, XQR_OVERFLOW);
             store_real<L>(p.norms + (int64_t)j * L, 1, nrm);
+            // the failure also travels in the norm (a NaN head): every CTA
+            // derives the pre-pass verdict from data fixed before the
+            // arrival barrier (p.key keeps changing after it)
+            if (bad) p.norms[(int64_t)j * L] = __longlong_as_double(0x7ff8000000000000ll);
         }
     }
     // grid-wide arrival (all CTAs are co-resident: cooperative launch)
@@ -320,6 +325,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
     }
     __syncthreads();
     R thr;
+    bool pre_err = false;  // every thread reads every norm: uniform
     {
         R best = rmake<R>(0.0);
         for (int j = 0; j < ncol; ++j) {
@@ -328,12 +334,12 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
             for (int l = 0; l < L; ++l) t[l] = __ldcg(p.norms + (int64_t)j * L + l);
             R v;
             load_real<L>(t, 1, v);
+            if (L > 1 && t[0] != t[0]) pre_err = true;  // (double is unchecked)
             if (lt(best, v)) best = v;
         }
         // breakdown_threshold (mgs.hpp:66-70)
         thr = mul(rmake<R>((double)m * real_of<L>::eps), best);
     }
-    const bool pre_err = __ldcg(p.key) != kNoError;
     // pivot flags: every CTA of the owner cluster adds 1 once q_j is out, or
     // kFlagErr + 1 if normalising column j failed in it; published when the
     // low half reaches cs.  A cluster stops only at a failed pivot's flag, so

@@ -67,10 +67,48 @@ def test_exit_codes(port, tmp_path):
     assert rc == 2
 
 
-def test_accuracy_csv():
-    rc, out, err = cli("accuracy", "--precision", "cdd", "--m", "8", "--n", "8", "--g", "1,8",
-                       "--trials", "10")
+def _fields(csv_text):
+    """rows without the wall_seconds column (timing differs by construction)"""
+    return [ln.split(",")[:-1] for ln in csv_text.splitlines()]
+
+
+@pytest.mark.parametrize("args,limbs,gs,trials,linear", [
+    (["--precision", "cdd", "--m", "8", "--n", "8", "--g", "1", "8", "--trials", "10"], 2, [1.0, 8.0], 10, False),
+    (["--precision", "cqd", "--m", "12", "--n", "9", "--g", "0", "--g", "17", "--g", "32",
+      "--trials", "7", "--seed", "5"], 4, [0.0, 17.0, 32.0], 7, False),
+    (["--precision", "cd", "--m", "10", "--n", "10", "--g", "1,16", "--trials", "5",
+      "--modulus-dist", "linear"], 1, [1.0, 16.0], 5, True),
+])
+def test_accuracy_csv_matches_reference(ref, args, limbs, gs, trials, linear):
+    """xqr_main.cpp:216-226: one sweep over every g (rows after the first draw
+    split(gi*trials + t)), the reference's accuracy_csv header and `accuracy,`
+    rows -- field for field against the reference's own sweep, except the
+    wall time."""
+    rc, out, err = cli("accuracy", *args)
     assert rc == 0, err
-    lines = out.splitlines()
-    assert lines[0] == "precision,m,n,g,trials,exclusions,m_e,M_e,D_e,wall_seconds"
-    assert len(lines) == 3 and lines[1].startswith("cdd,8,8,1,10,0,")
+    m, n = int(args[args.index("--m") + 1]), int(args[args.index("--n") + 1])
+    seed = int(args[args.index("--seed") + 1]) if "--seed" in args else 1
+    want, wrc = ref.accuracy_csv(limbs, m, n, gs, trials, seed, linear)
+    assert wrc == 0
+    assert out.splitlines()[0] == "kind,precision,m,n,g,trials,exclusions,m_e,M_e,D_e,wall_seconds"
+    assert _fields(out) == _fields(want)
+
+
+@pytest.mark.parametrize("prec,limbs,m,g,trials", [("cd", 1, 8, 16.0, 50), ("cdd", 2, 16, 64.0, 50),
+                                                     ("cd", 1, 32, 100.0, 20)])
+def test_accuracy_breakdowns_excluded_like_reference(ref, prec, limbs, m, g, trials):
+    """Wide magnitude ranges make near-singular matrices: breakdowns are
+    counted as exclusions exactly as the reference's trial loop counts them
+    (cd 8x8 g=16: 6 of 50; cdd 16x16 g=64: 26 of 50; cd 32x32 g=100: all, so
+    m_e / M_e / D_e are nan)."""
+    rc, out, err = cli("accuracy", "--precision", prec, "--m", str(m), "--n", str(m), "--g", str(g),
+                       "--trials", str(trials))
+    assert rc == 0, err
+    want, _ = ref.accuracy_csv(limbs, m, m, [g], trials)
+    assert _fields(out) == _fields(want)
+    assert int(_fields(out)[1][6]) > 0
+
+
+def test_accuracy_requires_precision():
+    rc, _, _ = cli("accuracy", "--m", "8", "--n", "8")
+    assert rc == 2

@@ -611,3 +611,36 @@ def test_tall_batch_device_api(port):
         x, z, _ = port.lsq_solve(A[s], B[s])
         assert_same(dx[s].cpu().numpy(), x, f"x[{s}]")
         assert_same(dz[s].cpu().numpy(), z, f"z[{s}]")
+
+
+# ---- routing when the persistent grid cannot be placed -----------------------------------
+@pytest.mark.parametrize("L,m,n", [(4, 64, 64), (4, 40, 33), (2, 96, 96), (2, 64, 20)])
+def test_grid_unplaceable_reroutes_to_cta(port, monkeypatch, L, m, n):
+    """XQR_GRID_MAX_SMS=0 emulates a device partition on which the cooperative
+    grid cannot be made co-resident: the single system is re-routed to the
+    one-CTA kernel (no error, same bits, counted in grid_fallbacks); with a
+    few SMs the grid runs narrower and still gives the same bits."""
+    a, b = port.gen_system(L, m, n, 1.0, 4400 + m + n)
+    x, z, st = port.lsq_solve(a, b)
+    q, r, st2 = port.mgs_qr(a)
+    assert st[0] == 0 and st2[0] == 0
+    ctx = xqr.context(0)
+    for sms, rerouted in (("0", True), ("3", False)):
+        monkeypatch.setenv("XQR_GRID_MAX_SMS", sms)
+        before = ctx.grid_fallbacks
+        gx, gz = xqr.lsq_solve(a, b)
+        gq, gr = xqr.mgs_qr(a)
+        assert_same(gx, x, f"x sms={sms}")
+        assert_same(gz, z, f"z sms={sms}")
+        assert_same(gq, q, f"q sms={sms}")
+        assert_same(gr, r, f"r sms={sms}")
+        assert (ctx.grid_fallbacks - before == 2) == rerouted
+
+
+def test_grid_unplaceable_tall_system_fails_loudly(port, monkeypatch):
+    """m > 1024 has no one-CTA kernel: an unplaceable grid is a cuda_error,
+    never a silent fallback."""
+    a, b = port.gen_system(4, 1100, 3, 1.0, 77)
+    monkeypatch.setenv("XQR_GRID_MAX_SMS", "0")
+    with pytest.raises(xqr.cuda_error):
+        xqr.lsq_solve(a, b)
