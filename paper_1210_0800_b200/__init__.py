@@ -30,6 +30,7 @@ memory image of ``col_matrix<R>``; a vector is ``(len, 2, L)``; a real is
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import threading
 
@@ -515,7 +516,9 @@ def accuracy_sweep(limbs: int, m: int = 32, n: int = 32, g_values=(1.0,), trials
             t = int(np.nonzero(bad)[0][0])
             code = int(codes[t]) if codes[t] != XQR_OK else int(ecodes[t])
             _raise(code, int(cols[t]), f"accuracy trial {t} (g={g})")
-        log10_e = np.log10(e[keep, 0])
+        # std::log10 of the leading limb (experiment.hpp:130): C libm's log10, as
+        # math.log10 calls it (numpy's vectorised log10 can differ by an ulp)
+        log10_e = np.array([math.log10(v) for v in e[keep, 0]], dtype=np.float64)
         rec = {"g": float(g), "m": m, "n": n, "limbs": limbs, "trials": int(keep.sum()),
                "exclusions": int((codes == XQR_BREAKDOWN).sum()), "log10_e": log10_e.tolist()}
         if len(log10_e):
