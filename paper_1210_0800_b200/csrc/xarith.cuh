@@ -1157,6 +1157,31 @@ XB_PAIR rpair<r4> mul2_r4(const r4 a1, const r4 b1, const r4 a2, const r4 b2) {
     }
     return o;
 }
+// x with its sign flipped when c (exact, as neg(): every limb's sign bit)
+XB_DEV r4 neg_if(const r4& x, bool c) {
+#ifdef __CUDA_ARCH__
+    const int f = c ? (int)0x80000000 : 0;
+    auto fl = [&](double v) { return __hiloint2double(__double2hiint(v) ^ f, __double2loint(v)); };
+    return {fl(x.c0), fl(x.c1), fl(x.c2), fl(x.c3)};
+#else
+    return c ? neg(x) : x;
+#endif
+}
+// One half of a complex product as ONE call: x1*y1 + (negate ? -(x2*y2) :
+// x2*y2) -- the real part (negate) or the imaginary part of cmul
+// (complex.hpp:41-44) with its operands chosen by the caller; the two
+// products in lockstep, then the sum.  The lane-pair batched kernel's leaf
+// and update (xpair.cuh): the products never cross a call boundary.
+XB_CALL_IF r4 hcmul_r4(const r4 x1, const r4 y1, const r4 x2, const r4 y2, const bool negate) {
+    r4 p1, p2;
+    bool k1, k2;
+    mul_fast2(x1, y1, x2, y2, p1, k1, p2, k2);
+    p2 = neg_if(p2, negate);
+    bool ok;
+    r4 r = add_fast(p1, p2, ok);
+    if (!ok) r = add_slow(p1, p2);
+    return r;
+}
 #if !(XB_CALLS & 4) || (XB_CALLS & 8) || (XB_CALLS & 16)
 template <>
 XB_DEV rpair<r4> add2<r4>(const r4& a1, const r4& b1, const r4& a2, const r4& b2) {

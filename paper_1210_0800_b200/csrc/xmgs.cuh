@@ -19,6 +19,7 @@
 #pragma once
 #include "xbacksub.cuh"
 #include "xcolumn.cuh"
+#include "xpair.cuh"
 #include "xqr_internal.h"
 
 namespace xb {
@@ -26,6 +27,7 @@ namespace xb {
 // LV = depth of the in-lane tree stack: rows-per-lane <= 2^(LV-1).
 template <int L, int LV>
 struct mgs_warp {
+    static constexpr int LIMBS = L;
     using R = real_t<L>;
     using C = cx<R>;
     using F = colfmt<L>;
@@ -99,13 +101,15 @@ struct mgs_warp {
     }
 };
 
-template <int L, int LV, int NW, bool LSQ, int MINB = 1>
+// W = the column primitives: mgs_warp<L, LV> (a lane per row group,
+// xcolumn.cuh) or mgs_pair<L> (a lane pair per row group, xpair.cuh).
+template <class W, int NW, bool LSQ, int MINB = 1>
 __global__ void __launch_bounds__(NW * 32, MINB) mgs_cta_kernel(SolveParams p, int rpl) {
-    using W = mgs_warp<L, LV>;
+    constexpr int L = W::LIMBS;
     using R = real_t<L>;
     using C = cx<R>;
     constexpr int L2 = 2 * L;
-    const colfmt<L> f(rpl);
+    const typename W::F f(rpl);
 
     extern __shared__ double smem[];  // two pivot slots of f.COL doubles
     __shared__ unsigned long long s_key;

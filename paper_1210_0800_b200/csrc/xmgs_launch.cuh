@@ -31,7 +31,7 @@ constexpr int min_blocks() {
 template <int L, int LV, bool LSQ>
 static cudaError_t launch_one(const SolveParams& p, int rpl, cudaStream_t s) {
     constexpr int NW = cta_warps<L, LV>();
-    auto kern = mgs_cta_kernel<L, LV, NW, LSQ, min_blocks<L, LV>()>;
+    auto kern = mgs_cta_kernel<mgs_warp<L, LV>, NW, LSQ, min_blocks<L, LV>()>;
     const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 32 * rpl);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -42,10 +42,37 @@ static cudaError_t launch_one(const SolveParams& p, int rpl, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Lane-pair primitives (xpair.cuh) for quad-double m <= 128: rows per pair
+// rpp = 16 pairs * rpp >= m.
+#ifndef XB_PAIR_WARPS
+#define XB_PAIR_WARPS 8
+#endif
+#ifndef XB_PAIR_MINB
+#define XB_PAIR_MINB 2
+#endif
+#ifndef XB_USE_PAIR
+#define XB_USE_PAIR 1
+#endif
+template <int L, bool LSQ>
+static cudaError_t launch_pair(const SolveParams& p, int rpp, cudaStream_t s) {
+    constexpr int NW = XB_PAIR_WARPS;
+    auto kern = mgs_cta_kernel<mgs_pair<L>, NW, LSQ, XB_PAIR_MINB>;
+    const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 16 * rpp);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<(unsigned)p.batch, NW * 32, smem, s>>>(p, rpp);
+    return cudaGetLastError();
+}
+
 // Stack depth 3 serves m <= 128 (the batched hot path) with the fewest
 // registers; depth 6 serves m <= 1024.
 template <int L, bool LSQ>
 static cudaError_t launch_rpl(const SolveParams& p, cudaStream_t s) {
+    if constexpr (L == 4 && XB_USE_PAIR)
+        if (p.m <= 128) return launch_pair<L, LSQ>(p, rows_per_pair(p.m), s);
     const int rpl = rows_per_lane(p.m);
     if (rpl <= 4) return launch_one<L, 3, LSQ>(p, rpl, s);
     if (rpl <= kMaxRowsPerLane) return launch_one<L, 6, LSQ>(p, rpl, s);

@@ -45,8 +45,16 @@ inline int rows_per_lane(int m) {
     return r;
 }
 constexpr int kMaxRowsPerLane = 32;  // m <= 1024
+// rows per lane PAIR (16 pairs per warp, xpair.cuh): quad-double m <= 128
+inline int rows_per_pair(int m) {
+    int r = 1;
+    while (16 * r < m) r <<= 1;
+    return r;
+}
 
-// doubles of planar workspace per system
+
+// doubles of planar workspace per system (32 x rows per lane per column;
+// also covers the lane-pair layout: 16 x rows_per_pair(m) <= 32 x rows_per_lane(m))
 inline int64_t ws_doubles(int limbs, int m, int ncols) {
     return (int64_t)ncols * 2 * limbs * 32 * rows_per_lane(m);
 }
