@@ -1,24 +1,30 @@
 #!/usr/bin/env python3
 """bench.py -- complex dd/qd MGS QR + least-squares solve on B200.
 
-Headline workload (BASELINE.json configs[4]): batched complex quad-double
-128x128 least-squares systems (a Newton-corrector batch), 4096 systems per
-GPU, inputs from the reference generator (experiment.hpp:64-79; system s of
-rank r draws from split_mix64(1).split(r*4096 + s)).  A "step" is one
-xqr_lsq_solve_batched_device launch over the rank's 4096 systems: MGS on
-[A b], y, z and the fused back substitution, all on the device.
+Headline workload (BASELINE.json configs[4]): a batch of 4096 independent
+complex quad-double 128x128 least-squares systems (a Newton-corrector batch)
+at 1/2/4/8 GPUs.  Default scaling is STRONG: the 4096 systems are the whole
+job, split into contiguous near-equal shards, rank r solving its shard with no
+collective (system s always draws split_mix64(1).split(s), experiment.hpp:64-79,
+so every N solves exactly the same systems).  --scaling weak gives every
+rank --batch systems.  A "step" is one xqr_lsq_solve_batched_device launch
+over the rank's shard: MGS on [A b], y, z and the fused back substitution.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Prints ONE JSON line (rank 0).  `value` = systems/s over all ranks, device-
-resident (inputs already in HBM; the 9.6 GB working set per GPU is larger
-than the 126 MB L2, so no explicit flush is needed); `e2e` = the same metric
-through the host-buffer C-ABI call (xqr_lsq_solve_batched: pinned staging,
-H2D of A and b, kernel, D2H of x, z and status inside the timed region).
-Also reported: the single-system latency configs (configs[1..3]), the FP64
-roofline of the solver kernel, the CPU baseline (the reference compiled from
-/root/reference, oracle/_ref, on this host's cores) and SM clocks sampled
-during the timed region.
+resident (inputs already in HBM; the working set is larger than the 126 MB
+L2, so no explicit flush is needed), timed with CUDA events and reduced with
+MAX over ranks; `e2e` = the same metric through the host-buffer C-ABI call
+(xqr_lsq_solve_batched: H2D of A and b, kernel, D2H of x, z and status inside
+the timed region).  Also reported at N = 1: the single-system latency configs
+(configs[1..3]: median of >= 20 device-resident launches after 3 warm-ups,
+the median host-buffer xqr_lsq_solve latency, the reference on one host core
+and its own par_lsq_solve on every core), the dd-vs-qd quality-up pair, the
+FP64 roofline of the solver kernel against the FP64 peak measured live on the
+same device, the CPU baseline (the reference compiled from /root/reference,
+oracle/_ref, on this host's cores, with its compiler, flags and CPU model) and
+SM clocks sampled during the timed region.
 """
 from __future__ import annotations
 
@@ -35,10 +41,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "batched complex qd MGS QR+solve (4096 x cqd 128x128 per GPU): systems/s"
+METRIC = "batched complex qd MGS QR+solve (4096 x cqd 128x128, configs[4]): systems/s"
 UNIT = "systems/s"
-FP64_PEAK_INSTR = 1.85e13  # measured FP64 lane-instr/s, profiles/r01_fp64_probe.log
-FP64_PEAK_FLOPS = 36.5e12  # measured DFMA FLOP/s (fma = 2), same probe
+# fallback FP64 peak (lane-instr/s, profiles/r01_fp64_probe.log) if the live
+# probe (xqr_fp64_peak, measured on the bench's own device) is unavailable
+FP64_PEAK_INSTR_FALLBACK = 1.85e13
 
 # FP64 work model: per-op instruction weights
 W_DD = dict(cmul=76, cadd=40, rdiv=110, sqrt=30, cdiv=417, fma_cmul=12)
@@ -54,6 +61,26 @@ def work_model(limbs: int, m: int, n: int):
     instr = (w["cmul"] * n_cmul + w["cadd"] * n_cadd + w["rdiv"] * n_rdiv + w["sqrt"] * n_sqrt
              + w["cdiv"] * n_cdiv)
     return float(instr), float(instr + w["fma_cmul"] * n_cmul)
+
+
+def host_info() -> dict:
+    """CPU model / cores of this host and the reference build the CPU arms load."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    info = {"cpu_model": model, "cores": os.cpu_count()}
+    try:
+        import oracle  # CPU baseline leg only
+
+        info["reference_build"] = oracle.reference_build()
+    except Exception as exc:  # noqa: BLE001
+        info["reference_build"] = {"unavailable": str(exc)}
+    return info
 
 
 # ---- clocks sampled during the timed region ----------------------------------------
@@ -110,12 +137,14 @@ class ClockSampler:
 
 def arm_config(args, world, per_rank):
     """The `config` both arms report (ours and --impl reference)."""
+    total = args.batch if args.scaling == "strong" else args.batch * world
     return {"workload": f"configs[4]: batched independent cqd {args.m}x{args.n} lsq_solve "
                         "(MGS on [A b] + back substitution)",
-            "systems_per_gpu": per_rank, "limbs": 4, "m": args.m, "n": args.n,
-            "generator": "experiment.hpp:64-79, g=1, split_mix64(1).split(rank*batch+s)",
-            "l2": "inputs (9.6 GB/GPU working set) larger than L2; no flush",
-            "parallelism": f"batch-sharded x{world}, no collective"}
+            "systems_total": total, "systems_per_gpu": per_rank, "scaling": args.scaling,
+            "limbs": 4, "m": args.m, "n": args.n,
+            "generator": "experiment.hpp:64-79, g=1, split_mix64(1).split(s), s = global system index",
+            "l2": "working set (inputs + 2.3 MB workspace per system) larger than L2; no flush",
+            "parallelism": f"batch-sharded x{world} (contiguous ranges), no collective"}
 
 
 # ---- the reference arm: the reference CPU implementation on this host ---------------
@@ -146,29 +175,38 @@ def cpu_reference_rate(limbs, m, n, sample, threads, seed=1, first_stream=0):
     return sample / dt, kind, dt
 
 
+CPU_SAMPLE = 256  # systems per timed reference step (a prefix of >= 256)
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    sample = max(threads, 16)
     rates = []
     kind = "port"
+    t_total = 0.0
     for step in range(args.warmup + args.steps):
+        # warm-up steps: one system per thread (caches, page faults); timed
+        # steps: the bounded sample, each on fresh systems of the workload
+        sample = threads if step < args.warmup else CPU_SAMPLE
         r, kind, dt = cpu_reference_rate(4, args.m, args.n, sample, threads,
-                                         first_stream=step * sample)
+                                         first_stream=(step * CPU_SAMPLE) % max(1, args.batch))
         if step >= args.warmup:
             rates.append(r)
+            t_total += dt
     value = float(np.mean(rates))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sample / value, "higher_is_better": True, "scaling": args.scaling,
+        "ms_per_step": 1e3 * CPU_SAMPLE / value, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64 (complex quad-double)", "data": "synthetic",
         "config": dict(arm_config(args, world, args.batch),
-                       reference_sample=f"{sample} systems per step (bounded CPU sample)"),
+                       reference_sample=f"{CPU_SAMPLE} systems per timed step (bounded CPU sample, "
+                                        "rate extrapolated to the batch)"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{sample} systems per step, sequential lsq_solve per system on "
-                                   f"{threads} threads"},
+                         "sample": f"{CPU_SAMPLE} cqd {args.m}x{args.n} systems per step, sequential "
+                                   f"lsq_solve per system on {threads} threads ({t_total:.1f} s)",
+                         "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -176,7 +214,14 @@ def run_reference_arm(args, rank, world):
 
 
 # ---- our arm ---------------------------------------------------------------------------
-def single_system_latency(xqr, ctx, torch, limbs, m, n, reps=2):
+def single_system_latency(xqr, ctx, torch, limbs, m, n, reps=20, warm=3, cpu=None):
+    """One single-system config (configs[1..3]): device-resident latency (the
+    device-pointer entry point; median of `reps` launches after `warm`
+    warm-ups, CUDA events on the ctx stream per launch), the host-buffer
+    xqr_lsq_solve latency (numpy in, numpy out: H2D, solve, D2H; median),
+    bitwise check against the reference's golden x, z, and -- with `cpu`
+    (the reference build) -- the reference's lsq_solve on one host core and
+    its par_lsq_solve on every core (parallel.hpp:105-153), timed once."""
     a, b = xqr.gen_systems(limbs, 1, m, n, 1.0, 1, -1)
     da = torch.from_numpy(a).cuda()
     db = torch.from_numpy(b).cuda()
@@ -185,15 +230,17 @@ def single_system_latency(xqr, ctx, torch, limbs, m, n, reps=2):
     dst = torch.zeros(2, dtype=torch.int64, device="cuda")
     call = lambda: ctx.lsq_solve_batched_device(limbs, 1, m, n, da.data_ptr(), db.data_ptr(),
                                                 dx.data_ptr(), dz.data_ptr(), dst.data_ptr())
-    call()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
+    for _ in range(warm):
         call()
-    e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for e0, e1 in ev:
+        e0.record()
+        call()
+        e1.record()
+    torch.cuda.synchronize()
+    times = sorted(e0.elapsed_time(e1) for e0, e1 in ev)
+    ms = float(np.median(times))
     instr, flops = work_model(limbs, m, n)
     golden = os.path.join(ROOT, "tests", "golden",
                           f"bench_{'cdd' if limbs == 2 else 'cqd'}_{m}x{n}.npz")
@@ -202,8 +249,34 @@ def single_system_latency(xqr, ctx, torch, limbs, m, n, reps=2):
         g = np.load(golden)
         parity = bool(np.array_equal(dx.cpu().numpy()[0].view(np.uint64), g["x"].view(np.uint64))
                       and np.array_equal(dz.cpu().numpy()[0].view(np.uint64), g["z"].view(np.uint64)))
-    return {"us_per_system": ms * 1e3, "fp64_gflops": flops / (ms * 1e-3) / 1e9,
-            "fp64_pipe_frac": instr / (ms * 1e-3) / FP64_PEAK_INSTR, "bitwise_vs_reference": parity}
+    # end to end through the host-buffer public API (xqr_lsq_solve)
+    for _ in range(warm):
+        xqr.lsq_solve(a[0], b[0])
+    e2e = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        hx, hz = xqr.lsq_solve(a[0], b[0])
+        e2e.append(time.perf_counter() - t0)
+    out = {"us_per_system": ms * 1e3, "us_min": times[0] * 1e3, "us_max": times[-1] * 1e3, "reps": reps,
+           "e2e_us": float(np.median(e2e)) * 1e6,
+           "fp64_gflops": flops / (ms * 1e-3) / 1e9,
+           "bitwise_vs_reference": parity,
+           "e2e_matches_device": bool(np.array_equal(hx.view(np.uint64), dx.cpu().numpy()[0].view(np.uint64)))}
+    out["_instr"] = instr
+    if cpu is not None:
+        ref, threads = cpu
+        t0 = time.perf_counter()
+        rx, rz, st = ref.lsq_solve(a[0], b[0])
+        out["cpu_ref_1core_us"] = (time.perf_counter() - t0) * 1e6
+        t0 = time.perf_counter()
+        px, pz, pst = ref.par_lsq_solve(a[0], b[0], threads)
+        out["cpu_ref_par_us"] = (time.perf_counter() - t0) * 1e6
+        out["cpu_ref_par_workers"] = threads
+        out["speedup_vs_cpu_1core"] = out["cpu_ref_1core_us"] / out["us_per_system"]
+        out["speedup_vs_cpu_par"] = out["cpu_ref_par_us"] / out["us_per_system"]
+        out["cpu_bitwise_equal"] = bool(np.array_equal(rx.view(np.uint64), hx.view(np.uint64))
+                                        and np.array_equal(px.view(np.uint64), hx.view(np.uint64)))
+    return out
 
 
 def main():
@@ -212,10 +285,11 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=4096, help="systems per GPU (weak scaling)")
+    ap.add_argument("--batch", type=int, default=4096,
+                    help="systems in the whole job (strong) or per GPU (weak)")
     ap.add_argument("--m", type=int, default=128)
     ap.add_argument("--n", type=int, default=128)
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-single", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -232,8 +306,8 @@ def main():
 
     import paper_1210_0800_b200 as xqr
 
-    # one GPU per rank; BENCH_DIST_BACKEND=gloo (dev) lets a one-GPU box run
-    # the N > 1 code path with every rank on the same device
+    # one GPU per rank; BENCH_DIST_BACKEND=gloo (dev / tests) lets a one-GPU
+    # box run the N > 1 code path with every rank on the same device
     backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
@@ -246,16 +320,26 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    from paper_1210_0800_b200.sharding import max_over_ranks, shard
+    from paper_1210_0800_b200.sharding import max_over_ranks, shard, sum_over_ranks
 
     limbs, m, n = 4, args.m, args.n
     first, per_rank = shard(args.batch, rank, world, args.scaling)
+    total_systems = args.batch * world if args.scaling == "weak" else args.batch
 
     ctx = xqr.Context(local)
     # one explicit stream shared by torch (events, copies) and the C ABI
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
+    # the FP64 roofline denominator, measured on this device before the run
+    try:
+        peak_instr = ctx.fp64_peak(0)
+        peak_flops = 2.0 * ctx.fp64_peak(1)
+        peak_source = "measured live on this device (xqr_fp64_peak: independent DADD / DFMA chains, " \
+                      "every SM; MEASURED_PEAKS.json has no FP64 entry)"
+    except Exception as exc:  # noqa: BLE001
+        peak_instr, peak_flops = FP64_PEAK_INSTR_FALLBACK, 2.0 * FP64_PEAK_INSTR_FALLBACK
+        peak_source = f"fallback profiles/r01_fp64_probe.log (live probe failed: {exc})"
     a, b = xqr.gen_systems(limbs, per_rank, m, n, 1.0, 1, first)
     da = torch.from_numpy(a).cuda()
     db = torch.from_numpy(b).cuda()
@@ -279,12 +363,10 @@ def main():
     clocks.start()
     launches0 = ctx.launch_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kern_ms = []
     barrier()
     e0.record()
     for _ in range(args.steps):
         step()
-        kern_ms.append(None)
     e1.record()
     barrier()
     clk = clocks.stop()
@@ -292,15 +374,14 @@ def main():
     ms = e0.elapsed_time(e1)
     last_kernel_ms = ctx.last_kernel_ms  # CUDA events around the last launch, ctx stream
     ms = max_over_ranks(ms, dist, red_dev)
-    total = (args.batch * world if args.scaling == "weak" else args.batch) * args.steps
-    value = total / (ms / 1e3)
+    value = total_systems * args.steps / (ms / 1e3)
 
     codes = dst.cpu().numpy()[:, 0] & 0xFFFFFFFF
-    n_fail = int((codes != 0).sum())
+    n_fail = int(sum_over_ranks(int((codes != 0).sum()), dist, red_dev))
     parity = None
     if rank == 0 and first == 0:
         ok = True
-        for s in range(4):
+        for s in range(min(4, per_rank)):
             g = os.path.join(ROOT, "tests", "golden", f"bench_cqd_{m}x{n}_s{s}.npz")
             if not os.path.exists(g):
                 ok = None
@@ -311,7 +392,8 @@ def main():
 
     # ---- e2e through the host-buffer public API ----------------------------------------
     # inputs sit in pinned host memory (the C ABI then DMAs them directly and
-    # pipelines the copies with the solves); x, z, status come back to host
+    # pipelines the copies with the solves, one kernel wave per chunk); x, z
+    # and the statuses come back to host memory inside the timed region
     a_pin = torch.from_numpy(a).pin_memory().numpy()
     b_pin = torch.from_numpy(b).pin_memory().numpy()
     xqr.lsq_solve_batched(a_pin, b_pin, device=local)  # warm the workspace
@@ -322,9 +404,12 @@ def main():
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     e2e_s = max_over_ranks(e2e_s, dist, red_dev)
-    e2e_value = (args.batch * world if args.scaling == "weak" else args.batch) / e2e_s
-    h2d = a.nbytes + b.nbytes
-    d2h = xh.nbytes + zh.nbytes + 16 * per_rank
+    e2e_value = total_systems / e2e_s
+    h2d = int(sum_over_ranks(a.nbytes + b.nbytes, dist, red_dev))
+    d2h = int(sum_over_ranks(xh.nbytes + zh.nbytes + 16 * per_rank, dist, red_dev))
+    e2e_bad = int(sum_over_ranks(int((ch != 0).sum()), dist, red_dev))
+    e2e_same = bool(np.array_equal(xh.view(np.uint64), dx.cpu().numpy().view(np.uint64)))
+    e2e_same = bool(sum_over_ranks(0 if e2e_same else 1, dist, red_dev) == 0)
 
     instr, flops = work_model(limbs, m, n)
     kernel_s = (last_kernel_ms or ms / args.steps) / 1e3
@@ -345,16 +430,24 @@ def main():
     single = {}
     cpu = None
     if rank == 0 and world == 1:
-        if not args.no_single:
-            for (L, mm, nn) in ((2, 256, 256), (4, 256, 256), (4, 512, 256)):
-                single[f"{'cdd' if L == 2 else 'cqd'}_{mm}x{nn}"] = single_system_latency(
-                    xqr, ctx, torch, L, mm, nn)
-            # quality-up (PAPER.md:791-797): cqd on the GPU vs cdd on one host
-            # core (the reference itself), same A and b, n = 80
+        threads = os.cpu_count() or 1
+        ref = None
+        if not args.no_cpu:
             try:
                 import oracle  # CPU baseline leg only
 
                 ref = oracle.reference() or oracle.port()
+            except Exception:  # noqa: BLE001
+                ref = None
+        if not args.no_single:
+            for (L, mm, nn) in ((2, 256, 256), (4, 256, 256), (4, 512, 256)):
+                r = single_system_latency(xqr, ctx, torch, L, mm, nn,
+                                          cpu=(ref, threads) if ref is not None else None)
+                r["fp64_pipe_frac"] = r.pop("_instr") / (r["us_per_system"] * 1e-6) / peak_instr
+                single[f"{'cdd' if L == 2 else 'cqd'}_{mm}x{nn}"] = r
+            # quality-up (PAPER.md:791-797): cqd on the GPU vs cdd on one host
+            # core (the reference itself), same A and b, n = 80
+            if ref is not None:
                 gq = single_system_latency(xqr, ctx, torch, 4, 80, 80)
                 a80, b80 = xqr.gen_systems(2, 1, 80, 80, 1.0, 1, -1)
                 t0 = time.perf_counter()
@@ -364,45 +457,41 @@ def main():
                     "gpu_cqd_us": gq["us_per_system"], "cpu_cdd_us_1core": cpu_ms * 1e3,
                     "speedup": cpu_ms * 1e3 / gq["us_per_system"],
                     "paper_c2050_vs_x5690": 3.08, "digits": "cqd ~62 vs cdd ~31"}
-            except Exception as exc:  # noqa: BLE001
-                single["quality_up_n80"] = {"unavailable": str(exc)}
-        if not args.no_cpu:
-            threads = os.cpu_count() or 1
-            sample = max(threads, 16)
+        if ref is not None:
             try:
-                rate, kind, dt = cpu_reference_rate(4, m, n, sample, threads)
+                rate, kind, dt = cpu_reference_rate(4, m, n, CPU_SAMPLE, threads)
                 cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
-                       "sample": f"{sample} cqd {m}x{n} systems (streams 0..{sample - 1}), "
+                       "sample": f"{CPU_SAMPLE} cqd {m}x{n} systems (streams 0..{CPU_SAMPLE - 1}), "
                                  f"sequential lsq_solve per system on {threads} threads, "
-                                 f"{dt:.1f} s wall"}
+                                 f"{dt:.1f} s wall; rate extrapolated to the batch",
+                       "host": host_info()}
             except Exception as exc:  # noqa: BLE001
                 cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
                        "sample": f"unavailable: {exc}"}
 
     if rank == 0:
+        waves = -(-per_rank // (2 * torch.cuda.get_device_properties(local).multi_processor_count))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64 (complex quad-double, 4 limbs)", "data": "synthetic",
-            "config": arm_config(args, world, per_rank),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
-                    "d2h_bytes_per_step": int(d2h * world),
+            "config": dict(arm_config(args, world, per_rank), kernel_waves_per_gpu=waves),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "xqr_lsq_solve_batched (pinned host A, b -> host x, z, status; "
                            "copies pipelined with the solves)",
-                    "e2e_bad_systems": int((ch != 0).sum()),
-                    "e2e_matches_device": bool(np.array_equal(xh.view(np.uint64),
-                                                              dx.cpu().numpy().view(np.uint64)))},
+                    "e2e_bad_systems": e2e_bad, "e2e_matches_device": e2e_same},
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp64", "achieved": achieved_instr / 1e12,
-                         "peak": FP64_PEAK_INSTR / 1e12, "unit": "T FP64 instr/s",
-                         "frac": achieved_instr / FP64_PEAK_INSTR, "traffic": traffic,
-                         "kernel": "mgs_cta_kernel<L=4,LV=3,NW=8,LSQ,MINB=2> (8 warps x 2 CTAs per SM)",
+                         "peak": peak_instr / 1e12, "unit": "T FP64 instr/s",
+                         "frac": achieved_instr / peak_instr, "traffic": traffic,
+                         "kernel": "mgs_cta_kernel<mgs_pair<4>, NW=8, LSQ, MINB=2> (lane-pair primitives, "
+                                   "8 warps x 2 CTAs per SM)",
                          "fp64_tflops": flops * per_rank / kernel_s / 1e12,
-                         "fp64_tflops_peak": FP64_PEAK_FLOPS / 1e12,
-                         "peak_source": "measured (profiles/r01_fp64_probe.log): MEASURED_PEAKS.json "
-                                        "has no FP64 entry",
-                         "work_per_system_instr": instr, "kernel_ms": kernel_s * 1e3,
+                         "fp64_tflops_peak": peak_flops / 1e12,
+                         "peak_source": peak_source,
+                         "work_per_system_instr": instr, "systems_per_launch": per_rank,
+                         "kernel_ms": kernel_s * 1e3,
                          "secondary": {"bound": "hbm", "unit": "GB/s", "peak": hbm_peak,
                                        "achieved": (traffic / kernel_s / 1e9) if traffic else None,
                                        "frac": (traffic / kernel_s / 1e9 / hbm_peak) if traffic else None,

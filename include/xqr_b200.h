@@ -151,6 +151,10 @@ int64_t xqr_ctx_launch_count(xqr_ctx* ctx);
  * kernels to the one-CTA kernel because the grid could not be made
  * co-resident (same results bit for bit; m <= 1024 only). */
 int64_t xqr_ctx_grid_fallbacks(xqr_ctx* ctx);
+/* FP64 roofline denominator measured on this ctx's device: lane
+ * instructions per second of independent DADD (op 0) or DFMA (op 1) chains
+ * over every SM (best of three launches). */
+int xqr_fp64_peak(xqr_ctx* ctx, int op, double* lane_instr_per_s);
 /* Accumulated device time (ms) of the most recent solver launch, measured
  * with CUDA events on the ctx stream (0 if not yet available). */
 float xqr_ctx_last_kernel_ms(xqr_ctx* ctx);

@@ -29,6 +29,34 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_LIB = os.path.join(HERE, "_build", "libxqr_oracle.so")
 REF_LIB = os.path.join(HERE, "_ref", "libxqr_ref.so")
+REF_LIB_V4 = os.path.join(HERE, "_ref", "libxqr_ref_v4.so")
+REF_BUILD_INFO = os.path.join(HERE, "_ref", "BUILD_INFO.json")
+
+
+def host_has_avx512() -> bool:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    fl = set(line.split(":", 1)[1].split())
+                    return {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl", "fma"} <= fl
+    except OSError:
+        pass
+    return False
+
+
+def reference_build() -> dict:
+    """Which reference build reference() loads here, with its compiler and flags."""
+    import json
+
+    info = {}
+    try:
+        info = json.load(open(REF_BUILD_INFO))
+    except (OSError, ValueError):
+        pass
+    v4 = os.path.exists(REF_LIB_V4) and host_has_avx512()
+    return {"lib": os.path.basename(REF_LIB_V4 if v4 else REF_LIB), "compiler": info.get("compiler"),
+            "flags": info.get("v4" if v4 else "portable")}
 REF_INC = "/root/reference/proj/include"
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -61,7 +89,8 @@ class Oracle:
 
     def __init__(self, kind: str = "port"):
         self.kind = kind
-        path = PORT_LIB if kind == "port" else REF_LIB
+        path = PORT_LIB if kind == "port" else (
+            REF_LIB_V4 if os.path.exists(REF_LIB_V4) and host_has_avx512() else REF_LIB)
         if not os.path.exists(path):
             raise FileNotFoundError(path)
         self.lib = ctypes.CDLL(path)

@@ -161,6 +161,7 @@ _SIGNATURES = {
                               _dp, _dp], _ci),
     "xqr_ctx_launch_count": ([_vp], _i64),
     "xqr_ctx_grid_fallbacks": ([_vp], _i64),
+    "xqr_fp64_peak": ([_vp, _ci, _dp], _ci),
     "xqr_ctx_last_kernel_ms": ([_vp], ctypes.c_float),
 }
 
@@ -225,6 +226,13 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(self._lib.xqr_ctx_launch_count(self.handle))
+
+    def fp64_peak(self, op: int = 0) -> float:
+        """Measured FP64 lane-instructions/s of this device (op 0: DADD, 1: DFMA)."""
+        v = ctypes.c_double()
+        rc = self._lib.xqr_fp64_peak(self.handle, op, ctypes.byref(v))
+        self.check(rc)
+        return float(v.value)
 
     @property
     def grid_fallbacks(self) -> int:
