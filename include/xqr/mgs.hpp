@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -18,6 +19,7 @@
 #include "xqr/errors.hpp"
 #include "xqr/matrix.hpp"
 #include "xqr/real_type.hpp"
+#include "xqr/reduction.hpp"
 #include "xqr_b200.h"
 
 namespace xqr {
@@ -33,6 +35,55 @@ struct lsq_solution {
     cvector<R> x;
     R residual_norm;
 };
+
+// The MGS building blocks of the reference (mgs.hpp:36-80), for callers that
+// drive their own factorisation loop (test_mgs.cpp:123-145,
+// acceptance.cpp:497-508).  They run on the host with the value types'
+// operators (the product's arithmetic, bitwise equal to the reference's);
+// mgs_qr / lsq_solve / back_substitute below are the B200 path.
+namespace detail {
+
+// sqrt of Re(a^H a): the imaginary part of a^H a is zero term by term
+template <class R>
+R column_norm(const cvector<R>& a, cvector<R>& scratch) {
+    return sqrt(tree_inner_product<R>(a, a, scratch).re);
+}
+
+// a /= ||a|| in place, returns r_kk; breakdown_error(column_index, 1-based)
+// when ||a|| <= threshold
+template <class R>
+R normalize_column(cvector<R>& a, cvector<R>& scratch, const R& threshold, std::size_t column_index) {
+    const R rkk = column_norm(a, scratch);
+    if (rkk <= threshold) throw breakdown_error(column_index);
+    for (auto& entry : a) entry = div_real(entry, rkk);
+    return rkk;
+}
+
+// r = q^H a, then a -= r q entry by entry; returns r
+template <class R>
+cplx<R> remove_projection(const cvector<R>& q, cvector<R>& a, cvector<R>& scratch) {
+    const cplx<R> r = tree_inner_product<R>(q, a, scratch);
+    for (std::size_t i = 0; i < a.size(); ++i) a[i] = a[i] - r * q[i];
+    return r;
+}
+
+// rows * epsilon * (largest column norm), in R
+template <class R>
+R breakdown_threshold(std::size_t rows, const R& max_column_norm) {
+    return R(static_cast<double>(rows) * real_traits<R>::epsilon) * max_column_norm;
+}
+
+template <class R>
+R max_column_norm(const std::vector<cvector<R>>& cols, cvector<R>& scratch) {
+    R best(0.0);
+    for (const auto& col : cols) {
+        const R v = column_norm(col, scratch);
+        if (v > best) best = v;
+    }
+    return best;
+}
+
+}  // namespace detail
 
 namespace device {
 
@@ -195,6 +246,28 @@ R residual_max_entry(const col_matrix<R>& a, const col_matrix<R>& q, const col_m
                                     ai.data(), qi.data(), ri.data(), reinterpret_cast<double*>(&out), &st);
     device::raise_status(rc, st);
     return out;
+}
+
+// mgs.hpp:183-204 -- residual_max_entry recomputed with every entry first
+// cast to W (real_cast: widening is exact): the same device metric, run in
+// W on the cast factors.
+template <class W, class R>
+W residual_max_entry_widened(const col_matrix<R>& a, const col_matrix<R>& q, const col_matrix<R>& r) {
+    const std::size_t m = a.rows(), n = a.cols();
+    if (q.rows() != m || q.cols() != n || r.rows() != n || r.cols() != n)
+        throw dimension_error("factor shapes do not match the input matrix");
+    if constexpr (std::is_same_v<W, R>) {
+        return residual_max_entry(a, q, r);
+    } else {
+        auto cast = [](const col_matrix<R>& x) {
+            col_matrix<W> out(x.rows(), x.cols());
+            for (std::size_t j = 0; j < x.cols(); ++j)
+                for (std::size_t i = 0; i < x.rows(); ++i)
+                    out(i, j) = cplx<W>{real_cast<W>(x(i, j).re), real_cast<W>(x(i, j).im)};
+            return out;
+        };
+        return residual_max_entry(cast(a), cast(q), cast(r));
+    }
 }
 
 // mgs.hpp:208-222 -- largest entry modulus of Q^H Q - I.
