@@ -217,6 +217,9 @@ XB_DEVICE bool cta_back_substitute(int n, const double* r, const double* y, doub
 // reference's.  xs (n*2L doubles), prep (n*(3L+1)) and sync (2 + NW ints)
 // are shared memory; blockDim.x is a multiple of 32, at least 64.  Returns
 // (uniformly) true on error.
+#ifndef XB_BS_ISOLATE
+#define XB_BS_ISOLATE 1
+#endif
 template <int L>
 XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, double* xs, double* prep,
                                     int* sync, unsigned long long* key, long long pos_base,
@@ -224,7 +227,21 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
     using R = real_t<L>;
     constexpr unsigned kFull = 0xffffffffu;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
-    const int part = lane & 1, pl = lane >> 1, NU = NW - 1, BW = 16 * NU;
+    // XB_BS_ISOLATE: the warps sharing the finisher's SM sub-partition (warp
+    // id = 0 mod 4) stay idle, so the sequential chain does not compete for
+    // that SMSP's FP64 issue; updater u runs on warp u + 1 + u / 3
+#if XB_BS_ISOLATE
+    const int NU = NW - (NW + 3) / 4;
+    const bool updater = warp > 0 && (warp & 3) != 0;
+    const int uo = warp - 1 - (warp >> 2);
+    auto uwarp = [](int u) { return u + 1 + u / 3; };
+#else
+    const int NU = NW - 1;
+    const bool updater = warp > 0;
+    const int uo = warp - 1;
+    auto uwarp = [](int u) { return u + 1; };
+#endif
+    const int part = lane & 1, pl = lane >> 1, BW = 16 * NU;
     const unsigned pmask = 3u << (lane & 30);
     volatile int* frontier = sync;  // lowest k whose x_k is final and in xs
     volatile int* stop = sync + 1;  // highest step at which an error occurred
@@ -295,7 +312,7 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
                 // dev instrumentation (XQR_GRID_TRACE): SM cycles per phase
                 unsigned long long c0 = trace ? clock64() : 0;
                 // x_{k-1} has every update but x_k's once its updater is past k+1
-                const int w = 1 + ((k - 1) >> 4) % NU;
+                const int w = uwarp(((k - 1) >> 4) % NU);
                 while (done[w] > k + 1 && *stop < k) __nanosleep(20);
                 __threadfence_block();
                 unsigned long long c1 = trace ? clock64() : 0, c2 = 0;
@@ -338,12 +355,12 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
                 }
             }
         }
-    } else {
+    } else if (updater) {
         // ---------------- updaters ----------------
-        const int base = 16 * (warp - 1) + pl;  // this pair's lowest unknown
+        const int base = 16 * uo + pl;  // this pair's lowest unknown
         int k = n - 1;
         for (; k >= 2; --k) {
-            if (16 * (warp - 1) > k - 2) break;  // every own unknown is past its updates
+            if (16 * uo > k - 2) break;  // every own unknown is past its updates
             if (lane == 0)
                 while (*frontier > k && *stop < k) __nanosleep(32);
             __syncwarp();
@@ -377,7 +394,7 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
         }
         __syncwarp();
         if (lane == 0 && k < 2) done[warp] = -1;  // nothing left: never hold the finisher
-        if (lane == 0 && k >= 2 && 16 * (warp - 1) > k - 2) done[warp] = -1;
+        if (lane == 0 && k >= 2 && 16 * uo > k - 2) done[warp] = -1;
     }
     return __syncthreads_or(err);
 }

@@ -59,6 +59,11 @@ XB_DEVICE void g2_red_release(int* p, int v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// the warp of each CTA that runs a pivot's scalar chain (sqrt, reciprocal)
+#ifndef XB_CHAIN_WARP
+#define XB_CHAIN_WARP 0
+#endif
+
 template <int L, int RPP>
 struct g2 {
     using R = real_t<L>;
@@ -360,7 +365,7 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
         // that shares the SM
         __shared__ double s_rkk[L], s_rc[L];
         __shared__ int s_code;
-        if (g.warp == 0) {
+        if (g.warp == XB_CHAIN_WARP) {
             R rkk0 = rsqrt_ref(s);
             if (tr) p.trace[j * 8 + 5] = g2_timer();
             int code0 = 0;

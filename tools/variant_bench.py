@@ -28,13 +28,17 @@ def main():
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--limbs", type=int, default=4)
     ap.add_argument("--qr", action="store_true")
+    ap.add_argument("--single", action="store_true",
+                    help="one system drawn from split_mix64(1) itself (the latency configs; grid kernels)")
     args = ap.parse_args()
     import torch
 
     import paper_1210_0800_b200 as xqr
 
     L, m, n, B = args.limbs, args.m, args.n, args.batch
-    a, b = xqr.gen_systems(L, B, m, n, 1.0, 1, 0)
+    if args.single:
+        B = 1
+    a, b = xqr.gen_systems(L, B, m, n, 1.0, 1, -1 if args.single else 0)
     ctx = xqr.Context(0)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -70,7 +74,12 @@ def main():
         h.update(dz.cpu().numpy().tobytes())
     codes = dst.cpu().numpy()[:, 0] & 0xFFFFFFFF
     golden = None
-    if not args.qr and L == 4 and m == 128 and n == 128:
+    gname = os.path.join(ROOT, "tests", "golden", f"bench_{'cdd' if L == 2 else 'cqd'}_{m}x{n}.npz")
+    if args.single and not args.qr and os.path.exists(gname):
+        g = np.load(gname)
+        golden = bool(np.array_equal(dx[0].cpu().numpy().view(np.uint64), g["x"].view(np.uint64))
+                      and np.array_equal(dz[0].cpu().numpy().view(np.uint64), g["z"].view(np.uint64)))
+    elif not args.qr and L == 4 and m == 128 and n == 128:
         golden = True
         for s in range(min(4, B)):
             g = np.load(os.path.join(ROOT, "tests", "golden", f"bench_cqd_128x128_s{s}.npz"))
