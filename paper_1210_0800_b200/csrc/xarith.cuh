@@ -619,6 +619,75 @@ XB_DEV r4 add_fast(const r4& a, const r4& b, bool& okr) {
     qadd_run<5>(q);
     return qadd_finish(q, okr);
 }
+// The level-paired fast path with the merge's output slots x[0..3] in memory
+// instead of registers (XB_XSMEM).  The register form writes each emitted
+// limb with a select per slot it could land in (x[k] for every k the step can
+// see: 18 double selects over the six steps, 7 more for the loop exit), which
+// made FSEL the second most executed instruction of the batched kernel after
+// DADD.  Here every step stores its candidate uu into the OPEN slot k (one
+// store; k advances when the reference emits), so a non-emitted candidate is
+// overwritten by the next emission or by the loop exit's x[k] = u -- exactly
+// the reference's x[k++] = d (quad_double.hpp:244-246) and x[k] = u,
+// x[++k] = v (:237-239).  Writes are monotone in k, so slots 2 and 3, zeroed
+// first, stay +0 unless reached, as x = {0, 0, 0, 0} does in the reference.
+// NT = the slot stride (threads sharing the slot array); slots 0..7 are
+// addressable (k <= 6 even when the fast path does not apply).
+template <int NT>
+XB_DEV void qadd_step_xs(double& u, double& v, double s, int& k, double* xs) {
+    double t, te, uu, ue;
+    two_sum(v, s, t, te);
+    two_sum(u, t, uu, ue);
+    const bool zb = (te != 0.0);
+    const bool emit = (ue != 0.0) && zb;
+    v = dsel(zb, te, ue);
+    u = dsel(emit, ue, uu);
+    xs[k * NT] = uu;
+    k += emit ? 1 : 0;
+}
+template <int NT>
+XB_DEV r4 add_fast_xs(const r4& a, const r4& b, bool& okr, double* xs) {
+    qadd_st q;
+    qadd_setup(a, b, q);
+    xs[2 * NT] = 0.0;
+    xs[3 * NT] = 0.0;
+    int k = 0;
+    qadd_step_xs<NT>(q.u, q.v, q.m2, k, xs);
+    qadd_step_xs<NT>(q.u, q.v, q.m3, k, xs);
+    qadd_step_xs<NT>(q.u, q.v, q.m4, k, xs);
+    qadd_step_xs<NT>(q.u, q.v, q.m5, k, xs);
+    qadd_step_xs<NT>(q.u, q.v, q.m6, k, xs);
+    const bool ok = q.ok && (k <= 3);  // the loop reaches its last step
+    qadd_step_xs<NT>(q.u, q.v, q.m7, k, xs);
+    // loop exit with everything consumed: x[k] = u; if (k < 3) x[k + 1] = v
+    // (k == 4: the loop left on its own condition, u and v are dropped)
+    xs[k * NT] = q.u;
+    if (k < 3) xs[(k + 1) * NT] = q.v;
+    const double x0 = xs[0], x1 = xs[NT], x2 = xs[2 * NT], x3 = xs[3 * NT];
+    double y0 = x0, y1 = x1, y2 = x2, y3 = x3;
+    bool okn;
+    renorm4_fast(y0, y1, y2, y3, okn);
+    okr = ok;
+    if (!okn) return renorm4_general(x0, x1, x2, x3);
+    return {y0, y1, y2, y3};
+}
+#ifndef XB_XSMEM
+#define XB_XSMEM 0
+#endif
+#if XB_XSMEM && defined(__CUDA_ARCH__)
+// one column of 8 slots per thread, CTAs of up to 256 threads
+constexpr int kXsThreads = 256;
+static __shared__ double xb_xslots[8][kXsThreads];
+XB_DEVICE r4 add_fast_any(const r4& a, const r4& b, bool& ok) {
+    return add_fast_xs<kXsThreads>(a, b, ok, &xb_xslots[0][threadIdx.x]);
+}
+#elif XB_XSMEM
+XB_DEV r4 add_fast_any(const r4& a, const r4& b, bool& ok) {
+    double xs[8];
+    return add_fast_xs<1>(a, b, ok, xs);
+}
+#else
+XB_DEV r4 add_fast_any(const r4& a, const r4& b, bool& ok) { return add_fast(a, b, ok); }
+#endif
 // two independent adds in lockstep
 XB_DEV void add_fast2(const r4& a1, const r4& b1, const r4& a2, const r4& b2, r4& o1, bool& k1,
                       r4& o2, bool& k2) {
@@ -850,7 +919,7 @@ XB_GEN r4 add_slow(const r4 a, const r4 b) {
 
 XB_OP4 r4 add(const r4 a, const r4 b) {
     bool ok;
-    r4 r = add_fast(a, b, ok);
+    r4 r = add_fast_any(a, b, ok);
     if (!ok) r = add_slow(a, b);
     return r;
 }
@@ -1178,7 +1247,7 @@ XB_CALL_IF r4 hcmul_r4(const r4 x1, const r4 y1, const r4 x2, const r4 y2, const
     mul_fast2(x1, y1, x2, y2, p1, k1, p2, k2);
     p2 = neg_if(p2, negate);
     bool ok;
-    r4 r = add_fast(p1, p2, ok);
+    r4 r = add_fast_any(p1, p2, ok);
     if (!ok) r = add_slow(p1, p2);
     return r;
 }

@@ -17,17 +17,19 @@ LIB = os.path.join(ROOT, "tests", "cpp", "_build", "libxarith_host.so")
 CSRC = os.path.join(ROOT, "paper_1210_0800_b200", "csrc")
 
 
-@pytest.fixture(scope="module", params=[0, 1], ids=["batched-build", "grid-build"])
+@pytest.fixture(scope="module", params=[0, 1, 2], ids=["batched-build", "grid-build", "register-build"])
 def host(request):
-    """The arithmetic as the batched kernels compile it, and as the
-    single-system kernels do (-DXB_SHIFT_TAIL=1: in-place leftover folds
-    after shifted merges)."""
-    lib_path = LIB if request.param == 0 else LIB.replace(".so", "_tail.so")
+    """The arithmetic as the batched kernels compile it (-DXB_XSMEM=1: the
+    merge's output slots in memory), as the single-system kernels do
+    (-DXB_SHIFT_TAIL=1: in-place leftover folds after shifted merges), and
+    the plain register form."""
+    lib_path = {0: LIB.replace(".so", "_xs.so"), 1: LIB.replace(".so", "_tail.so"), 2: LIB}[request.param]
+    flags = {0: ["-DXB_XSMEM=1"], 1: ["-DXB_SHIFT_TAIL=1"], 2: []}[request.param]
     deps = [SRC] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.startswith("xarith")]
     if not os.path.exists(lib_path) or os.path.getmtime(lib_path) < max(os.path.getmtime(d) for d in deps):
         os.makedirs(os.path.dirname(lib_path), exist_ok=True)
         subprocess.run(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-shared", "-fPIC",
-                        f"-DXB_SHIFT_TAIL={request.param}", SRC, "-o", lib_path], check=True)
+                        *flags, SRC, "-o", lib_path], check=True)
     lib = ctypes.CDLL(lib_path)
     dp = ctypes.POINTER(ctypes.c_double)
     lib.xh_arith.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, dp, dp, dp,
