@@ -1044,7 +1044,14 @@ XB_OP4 r4 mul(const r4 a, const r4 b) {
 // Always-call forms of the qd add / multiply, for the latency-bound scalar
 // chains (Newton iterations, reduction trees, pivot divisions): one shared
 // copy of each operation stays hot in the instruction cache of a lone warp.
-XB_CALL_IF r4 addc(const r4 a, const r4 b) { return add(a, b); }
+// (when add / mul are calls already -- XB_CALLS & 4 -- these are the same
+// calls, not a second call layer around them)
+#if (XB_CALLS & 4)
+#define XB_CALLC XB_DEV
+#else
+#define XB_CALLC XB_CALL_IF
+#endif
+XB_CALLC r4 addc(const r4 a, const r4 b) { return add(a, b); }
 // the Newton sites where the operands are known to merge unevenly (a
 // constant 1.0 or seed with zero lower limbs, a correction several limbs
 // down): try the alternative fixed merges first
@@ -1057,7 +1064,7 @@ XB_CALL_IF r4 addz(const r4 a, const r4 b) {
     return add_merge_pred(a, b);
 }
 XB_DEV r4 subz(const r4& a, const r4& b) { return addz(a, neg(b)); }
-XB_CALL_IF r4 mulc(const r4 a, const r4 b) { return mul(a, b); }
+XB_CALLC r4 mulc(const r4 a, const r4 b) { return mul(a, b); }
 XB_DEV r4 subc(const r4& a, const r4& b) { return addc(a, neg(b)); }
 XB_DEV r1 addc(const r1& a, const r1& b) { return add(a, b); }
 XB_DEV r2 addc(const r2& a, const r2& b) { return add(a, b); }
@@ -1241,7 +1248,7 @@ XB_DEV r4 neg_if(const r4& x, bool c) {
 // (complex.hpp:41-44) with its operands chosen by the caller; the two
 // products in lockstep, then the sum.  The lane-pair batched kernel's leaf
 // and update (xpair.cuh): the products never cross a call boundary.
-XB_CALL_IF r4 hcmul_r4(const r4 x1, const r4 y1, const r4 x2, const r4 y2, const bool negate) {
+XB_DEV r4 hcmul_inl(const r4& x1, const r4& y1, const r4& x2, const r4& y2, const bool negate) {
     r4 p1, p2;
     bool k1, k2;
     mul_fast2(x1, y1, x2, y2, p1, k1, p2, k2);
@@ -1250,6 +1257,9 @@ XB_CALL_IF r4 hcmul_r4(const r4 x1, const r4 y1, const r4 x2, const r4 y2, const
     r4 r = add_fast_any(p1, p2, ok);
     if (!ok) r = add_slow(p1, p2);
     return r;
+}
+XB_CALL_IF r4 hcmul_r4(const r4 x1, const r4 y1, const r4 x2, const r4 y2, const bool negate) {
+    return hcmul_inl(x1, y1, x2, y2, negate);
 }
 #if !(XB_CALLS & 4) || (XB_CALLS & 8) || (XB_CALLS & 16)
 template <>

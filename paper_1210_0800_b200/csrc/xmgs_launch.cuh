@@ -33,7 +33,7 @@ static cudaError_t launch_one(const SolveParams& p, int rpl, cudaStream_t s) {
     constexpr int NW = cta_warps<L, LV>();
     auto kern = mgs_cta_kernel<mgs_warp<L, LV>, NW, LSQ, min_blocks<L, LV>()>;
     const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 32 * rpl);
-    if (smem > 48 * 1024) {
+    if (smem > 16 * 1024) {  // with the static shared memory above 48 KB
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
@@ -58,7 +58,7 @@ static cudaError_t launch_pair(const SolveParams& p, int rpp, cudaStream_t s) {
     constexpr int NW = XB_PAIR_WARPS;
     auto kern = mgs_cta_kernel<mgs_pair<L>, NW, LSQ, XB_PAIR_MINB>;
     const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 16 * rpp);
-    if (smem > 48 * 1024) {
+    if (smem > 16 * 1024) {  // with the static shared memory above 48 KB
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;

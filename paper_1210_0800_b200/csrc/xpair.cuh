@@ -33,7 +33,7 @@ namespace xb {
 #endif
 // prefetch each column task's column into L1 at the start of the task
 #ifndef XB_PAIR_L1PF
-#define XB_PAIR_L1PF 0
+#define XB_PAIR_L1PF 1
 #endif
 // leaf / update as one call each (hcmul_r4: both products and their sum)
 #ifndef XB_PAIR_HCMUL
