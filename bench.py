@@ -485,8 +485,8 @@ def main():
             "roofline": {"bound": "fp64", "achieved": achieved_instr / 1e12,
                          "peak": peak_instr / 1e12, "unit": "T FP64 instr/s",
                          "frac": achieved_instr / peak_instr, "traffic": traffic,
-                         "kernel": "mgs_cta_kernel<mgs_pair<4>, NW=8, LSQ, MINB=2> (lane-pair primitives, "
-                                   "8 warps x 2 CTAs per SM)",
+                         "kernel": "mgs_cta_kernel<mgs_pair<4>, NW=12, LSQ, MINB=2> (lane-pair primitives, "
+                                   "12 warps x 2 CTAs per SM, 80 registers)",
                          "fp64_tflops": flops * per_rank / kernel_s / 1e12,
                          "fp64_tflops_peak": peak_flops / 1e12,
                          "peak_source": peak_source,

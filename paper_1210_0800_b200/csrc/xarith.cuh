@@ -673,9 +673,12 @@ XB_DEV r4 add_fast_xs(const r4& a, const r4& b, bool& okr, double* xs) {
 #ifndef XB_XSMEM
 #define XB_XSMEM 0
 #endif
+// one column of 8 slots per thread, CTAs of up to XB_XS_THREADS threads
+#ifndef XB_XS_THREADS
+#define XB_XS_THREADS 384
+#endif
 #if XB_XSMEM && defined(__CUDA_ARCH__)
-// one column of 8 slots per thread, CTAs of up to 256 threads
-constexpr int kXsThreads = 256;
+constexpr int kXsThreads = XB_XS_THREADS;
 static __shared__ double xb_xslots[8][kXsThreads];
 XB_DEVICE r4 add_fast_any(const r4& a, const r4& b, bool& ok) {
     return add_fast_xs<kXsThreads>(a, b, ok, &xb_xslots[0][threadIdx.x]);

@@ -28,24 +28,36 @@ constexpr int min_blocks() {
     return L == 4 ? (LV <= 3 ? XB_MINB4 : 1) : (LV <= 3 ? 4 : 2);
 }
 
+// Opt a kernel in to `bytes` of dynamic shared memory (idempotent; the
+// largest size requested so far is remembered per kernel).
+template <class K>
+static cudaError_t allow_dynamic_smem(K kern, size_t bytes) {
+    static size_t allowed = 0;
+    if (bytes <= allowed) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) allowed = bytes;
+    return e;
+}
+
 template <int L, int LV, bool LSQ>
 static cudaError_t launch_one(const SolveParams& p, int rpl, cudaStream_t s) {
     constexpr int NW = cta_warps<L, LV>();
     auto kern = mgs_cta_kernel<mgs_warp<L, LV>, NW, LSQ, min_blocks<L, LV>()>;
     const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 32 * rpl);
-    if (smem > 16 * 1024) {  // with the static shared memory above 48 KB
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-    }
+    // static (the qd add's slots) + dynamic shared memory may exceed 48 KB
+    if (cudaError_t e = allow_dynamic_smem(kern, smem)) return e;
     kern<<<(unsigned)p.batch, NW * 32, smem, s>>>(p, rpl);
     return cudaGetLastError();
 }
 
 // Lane-pair primitives (xpair.cuh) for quad-double m <= 128: rows per pair
-// rpp = 16 pairs * rpp >= m.
+// rpp = 16 pairs * rpp >= m.  12 warps x 2 CTAs per SM (80 registers, the
+// caller-saved values around the qd calls spill): 24 warps hide more of the
+// qd add's dependent-DADD latency than 16 warps at 128 registers -- measured
+// on 4096 x cqd 128x128: 8 warps 4,520 sys/s, 12 4,621, 14 4,572, 16 4,353;
+// 8 warps x 3 CTAs 4,610, 6 x 4 4,458, 8 x 4 4,236.
 #ifndef XB_PAIR_WARPS
-#define XB_PAIR_WARPS 8
+#define XB_PAIR_WARPS 12
 #endif
 #ifndef XB_PAIR_MINB
 #define XB_PAIR_MINB 2
@@ -56,13 +68,13 @@ static cudaError_t launch_one(const SolveParams& p, int rpl, cudaStream_t s) {
 template <int L, bool LSQ>
 static cudaError_t launch_pair(const SolveParams& p, int rpp, cudaStream_t s) {
     constexpr int NW = XB_PAIR_WARPS;
+#if XB_XSMEM
+    static_assert(NW * 32 <= XB_XS_THREADS, "the qd add's shared-memory slots (xarith.cuh) cover every thread");
+#endif
     auto kern = mgs_cta_kernel<mgs_pair<L>, NW, LSQ, XB_PAIR_MINB>;
     const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 16 * rpp);
-    if (smem > 16 * 1024) {  // with the static shared memory above 48 KB
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-    }
+    // static (the qd add's slots) + dynamic shared memory may exceed 48 KB
+    if (cudaError_t e = allow_dynamic_smem(kern, smem)) return e;
     kern<<<(unsigned)p.batch, NW * 32, smem, s>>>(p, rpp);
     return cudaGetLastError();
 }
