@@ -28,11 +28,10 @@ constexpr int min_blocks() {
     return L == 4 ? (LV <= 3 ? XB_MINB4 : 1) : (LV <= 3 ? 4 : 2);
 }
 
-// Opt a kernel in to `bytes` of dynamic shared memory (idempotent; the
-// largest size requested so far is remembered per kernel).
+// Opt a kernel in to `bytes` of dynamic shared memory; `allowed` (one per
+// kernel instance, kept by the caller) remembers the largest size granted.
 template <class K>
-static cudaError_t allow_dynamic_smem(K kern, size_t bytes) {
-    static size_t allowed = 0;
+static cudaError_t allow_dynamic_smem(K kern, size_t bytes, size_t& allowed) {
     if (bytes <= allowed) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e == cudaSuccess) allowed = bytes;
@@ -45,7 +44,8 @@ static cudaError_t launch_one(const SolveParams& p, int rpl, cudaStream_t s) {
     auto kern = mgs_cta_kernel<mgs_warp<L, LV>, NW, LSQ, min_blocks<L, LV>()>;
     const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 32 * rpl);
     // static (the qd add's slots) + dynamic shared memory may exceed 48 KB
-    if (cudaError_t e = allow_dynamic_smem(kern, smem)) return e;
+    static size_t allowed = 0;  // per template instance = per kernel
+    if (cudaError_t e = allow_dynamic_smem(kern, smem, allowed)) return e;
     kern<<<(unsigned)p.batch, NW * 32, smem, s>>>(p, rpl);
     return cudaGetLastError();
 }
@@ -74,7 +74,8 @@ static cudaError_t launch_pair(const SolveParams& p, int rpp, cudaStream_t s) {
     auto kern = mgs_cta_kernel<mgs_pair<L>, NW, LSQ, XB_PAIR_MINB>;
     const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 16 * rpp);
     // static (the qd add's slots) + dynamic shared memory may exceed 48 KB
-    if (cudaError_t e = allow_dynamic_smem(kern, smem)) return e;
+    static size_t allowed = 0;  // per template instance = per kernel
+    if (cudaError_t e = allow_dynamic_smem(kern, smem, allowed)) return e;
     kern<<<(unsigned)p.batch, NW * 32, smem, s>>>(p, rpp);
     return cudaGetLastError();
 }
