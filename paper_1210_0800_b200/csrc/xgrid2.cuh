@@ -650,10 +650,13 @@ cudaError_t launch_grid2_t(const GridParams& p, int max_clusters, cudaStream_t s
         // CTAs per SM (kGrid2PerSM; XQR_GRID_PER_SM overrides, dev only)
         const char* e = std::getenv("XQR_GRID_PER_SM");
         const int per_sm = e ? std::max(1, std::atoi(e)) : kGrid2PerSM;
-        const size_t floor_b = per_sm == 1 ? 120 * 1024 : (per_sm == 2 ? 100 * 1024 : 60 * 1024);
+        size_t floor_b = per_sm == 1 ? 120 * 1024 : (per_sm == 2 ? 100 * 1024 : 60 * 1024);
+        // the floor counts the kernel's static shared memory too
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) floor_b -= std::min(floor_b, fa.sharedSizeBytes);
         if (cfg.dynamicSmemBytes < floor_b) cfg.dynamicSmemBytes = floor_b;
     }
-    if (cfg.dynamicSmemBytes > 48 * 1024) {
+    {  // (static + dynamic may pass 48 KB even when the dynamic part does not)
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)cfg.dynamicSmemBytes);
         if (e != cudaSuccess) return e;
@@ -689,7 +692,7 @@ template <int L>
 cudaError_t launch_grid2_backsub(const GridParams& p, cudaStream_t s) {
     auto bs = grid2_backsub_kernel<L>;
     const size_t bsmem = g2_backsub_smem<L>(p.n);
-    if (bsmem > 48 * 1024) {
+    {  // (static + dynamic may pass 48 KB even when the dynamic part does not)
         cudaError_t e = cudaFuncSetAttribute(bs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
         if (e != cudaSuccess) return e;
     }
