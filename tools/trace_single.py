@@ -40,13 +40,16 @@ def main():
         if pre_end and start:
             print(f"  pre-pass (column norms + threshold) {(pre_end - start) / 1e3:.1f} us")
         if args.pivots and args.limbs <= 2:
-            # xgrid1 stamps: 0 q_{j-1} in hand, 1 column j updated, 2 published
+            # xgrid1 stamps: 0 q_{j-1} in hand, 1 column j updated, 4 norm tree,
+            # 5 sqrt, 6 reciprocal, 7 divided, 2 published
             T = t[:, 1:9].astype(np.int64)
-            rows = [[T[j][0] - T[j - 1][2], T[j][1] - T[j][0], T[j][2] - T[j][1]]
-                    for j in range(2, args.n - 1) if min(T[j][0], T[j][1], T[j][2], T[j - 1][2]) > 0]
+            rows = [[T[j][0] - T[j - 1][2], T[j][1] - T[j][0], T[j][4] - T[j][1], T[j][5] - T[j][4],
+                     T[j][6] - T[j][5], T[j][7] - T[j][6], T[j][2] - T[j][7]]
+                    for j in range(2, args.n - 1) if min(T[j][0], T[j][1], T[j][2], T[j][7], T[j - 1][2]) > 0]
             if rows:
                 avg = np.array(rows, dtype=np.float64).mean(axis=0) / 1e3
-                print("  dd pivots: handoff %.2f, update %.2f, normalise+publish %.2f us" % tuple(avg))
+                print("  dd pivots: handoff %.2f, update %.2f, normtree %.2f, sqrt %.2f, recip %.2f, "
+                      "divide %.2f, publish %.2f us" % tuple(avg))
         elif args.pivots:
             # per pivot j (row j of the trace, globaltimer ns): 0 q_{j-1} in hand,
             # 1 column j updated, 4 norm tree, 5 sqrt, 6 reciprocal, 7 divided,
