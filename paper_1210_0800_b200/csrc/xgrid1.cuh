@@ -286,6 +286,8 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
             C r = cta_tree<LV, C>(m, f.rpt, red_c, [&](int i) {
                 return cmul(cconj(f.load(smem, i, tid)), f.load(col, i, tid));
             });
+            // dev trace: the critical update's dot product done (second stamp block)
+            if (p.trace && tid == 0 && j == k + 1) p.trace[8 * (n + 1) + 8 * (k + 1)] = gtimer();
             bool ok = cfinite(r);
             for (int i = 0; i < f.rpt; ++i) {
                 if (tid * f.rpt + i < m) {

@@ -50,6 +50,11 @@ def main():
                 avg = np.array(rows, dtype=np.float64).mean(axis=0) / 1e3
                 print("  dd pivots: handoff %.2f, update %.2f, normtree %.2f, sqrt %.2f, recip %.2f, "
                       "divide %.2f, publish %.2f us" % tuple(avg))
+            if args.split:
+                D = t[:, 9].astype(np.int64)  # dot product of the critical update done
+                sp = [[D[j] - T[j][0], T[j][1] - D[j]] for j in range(2, args.n - 1) if min(D[j], T[j][0], T[j][1]) > 0]
+                if sp:
+                    print("  update split (us): dot %.2f, axpy+sync %.2f" % tuple(np.array(sp, dtype=np.float64).mean(axis=0) / 1e3))
         elif args.pivots:
             # per pivot j (row j of the trace, globaltimer ns): 0 q_{j-1} in hand,
             # 1 column j updated, 4 norm tree, 5 sqrt, 6 reciprocal, 7 divided,
