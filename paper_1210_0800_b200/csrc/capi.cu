@@ -171,6 +171,8 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     if (limbs <= 2) {
         p.cs = 1;
         p.rpt = xb::grid1_rows_per_thread(m);
+        p.chain = 1;
+        if (const char* e = std::getenv("XQR_GRID_CHAIN")) p.chain = std::atoi(e);  // dev
     } else {
         xb::grid_shape(m, p.cs, p.rpt, p.pair_bulk);
         if (const char* e = std::getenv("XQR_GRID_PAIR")) p.pair_bulk = std::atoi(e);  // dev
@@ -191,7 +193,7 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     const size_t o_ws = plan.add(sizeof(double) * grid_ws_doubles(limbs, m, ncol));
     const size_t o_rws = plan.add(lsq ? sizeof(double) * xb::rws_doubles(limbs, n) : 0);
     const size_t o_nrm = plan.add(sizeof(double) * (size_t)ncol * limbs);
-    const size_t o_flg = plan.add(sizeof(int) * ((size_t)n + 4));
+    const size_t o_flg = plan.add(sizeof(int) * ((size_t)n + 4 + ncol));
     const size_t o_key = plan.add(sizeof(unsigned long long));
     const char* trace_path = std::getenv("XQR_GRID_TRACE");  // dev instrumentation
     const size_t o_trc = plan.add(trace_path ? sizeof(unsigned long long) * 16 * (size_t)(n + 1) : 0);
@@ -202,9 +204,10 @@ int solve_grid(xqr_ctx* ctx, bool lsq, int limbs, int m, int n, const double* d_
     p.norms = reinterpret_cast<double*>(at(ctx, scratch_off + o_nrm));
     p.flags = reinterpret_cast<int*>(at(ctx, scratch_off + o_flg));
     p.counters = p.flags + n;
+    p.cflags = p.counters + 4;
     p.key = reinterpret_cast<unsigned long long*>(at(ctx, scratch_off + o_key));
     p.trace = trace_path ? reinterpret_cast<unsigned long long*>(at(ctx, scratch_off + o_trc)) : nullptr;
-    cudaMemsetAsync(p.flags, 0, sizeof(int) * ((size_t)n + 4), ctx->stream);
+    cudaMemsetAsync(p.flags, 0, sizeof(int) * ((size_t)n + 4 + ncol), ctx->stream);
     cudaMemsetAsync(p.key, 0xFF, sizeof(unsigned long long), ctx->stream);
     if (p.trace) cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * 16 * (size_t)(n + 1), ctx->stream);
     int per_sm = limbs == 4 ? xb::kGrid2PerSM : 1;

@@ -24,6 +24,7 @@
 // keep the reference's first-in-program-order semantics (status_key).
 #pragma once
 #include <cooperative_groups.h>
+#include <cuda_pipeline.h>
 
 #include "xbacksub.cuh"
 #include "xcolumn.cuh"
@@ -112,6 +113,21 @@ XB_DEVICE void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Two columns' values in one tree pass (the chain mode's bulk CTAs update
+// their columns in pairs: both reductions share every level's latency).
+template <class C>
+struct cpair {
+    C x, y;
+};
+template <class C>
+XB_DEVICE cpair<C> vadd(const cpair<C>& a, const cpair<C>& b) {
+    return {vadd(a.x, b.x), vadd(a.y, b.y)};
+}
+template <class C>
+XB_DEVICE cpair<C> vshfl_down(const cpair<C>& v, int o) {
+    return {vshfl_down(v.x, o), vshfl_down(v.y, o)};
+}
+
 template <int L, int LV, bool LSQ>
 __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p) {
     namespace cg = cooperative_groups;
@@ -125,6 +141,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
 
     extern __shared__ double smem[];  // q_k staging: f.COL doubles
     __shared__ C red_c[kGridWarps + 1];
+    __shared__ cpair<C> red_p[kGridWarps + 1];
     __shared__ R red_r[kGridWarps + 1];
     __shared__ R s_thr;
     __shared__ int s_flag;
@@ -132,6 +149,18 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
     double* rdst = LSQ ? p.rws : p.r;
     double* ydst = LSQ ? p.rws + (int64_t)n * n * L2 : nullptr;
     auto colp = [&](int j) { return p.ws + (int64_t)j * f.COL; };
+    // Column ownership.  Cyclic mode: column j -> CTA j mod G, whose owner of
+    // column k+1 updates it first in round k and normalises it.  Chain mode
+    // (p.chain, G >= 3): CTA 0 owns no column but runs EVERY pivot -- the
+    // last projection of column k+1 with q_k still in its shared memory, and
+    // the normalisation -- alone on its SM, while CTAs 1.. own the columns
+    // (j -> 1 + j mod (G-1)) and apply every earlier projection, reporting
+    // each through p.cflags.  The chain then never waits for a pivot's
+    // hand-off between CTAs.
+    const bool chain = p.chain != 0 && G >= 3;
+    const int S = chain ? G - 1 : G;         // ownership stride
+    const int own0 = chain ? c - 1 : c;      // first owned column (< 0: none)
+    const bool bulk = own0 >= 0;
 
     auto col_sq = [&](const double* col) {
         return cta_tree<LV, R>(m, f.rpt, red_r, [&](int i) {
@@ -144,7 +173,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
     };
 
     // ---- pack owned columns AoS -> planar; QR: zero the strict lower R -----
-    for (int j = c; j < ncol; j += G) {
+    for (int j = bulk ? own0 : ncol; j < ncol; j += S) {
         const double* src = (j < n) ? p.a + (int64_t)j * m * L2 : p.b;
         double* dst = colp(j);
         for (int e = tid; e < m * L2; e += kGridThreads) {
@@ -158,7 +187,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
     __syncthreads();
 
     // ---- norm pre-pass (mgs.hpp:91-96 / :143) ----------------------------------
-    for (int j = c; j < ncol; j += G) {
+    for (int j = bulk ? own0 : ncol; j < ncol; j += S) {
         R s = col_sq(colp(j));
         R nrm = rsqrt_ref(s);
         const bool bad = !vfinite(s) || !vfinite(nrm);
@@ -207,9 +236,34 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
     const R thr = s_thr;
     const bool pre_err = __syncthreads_or(pre_bad) != 0;  // grid-uniform: read from the norms
 
+    // Chain mode: the next pivot column's own rows are copied into the spare
+    // buffer with cp.async while the current pivot runs its scalar chain --
+    // by each thread for its own rows, as soon as it sees the column's
+    // earlier projections done (one acquire poll; if not yet, it loads them
+    // itself when the pivot starts).  No other thread reads those rows.
+    double* sc = smem + f.COL;            // the current pivot column
+    double* sn = smem + 2 * (size_t)f.COL;  // the next one, in flight
+    bool pref = false;
+    auto chain_prefetch = [&](int jn) {
+        pref = false;
+        if (jn >= n || ld_acquire(p.cflags + jn) < jn - 1) return;
+        const double* src = colp(jn);
+        for (int i = 0; i < f.rpt; ++i)
+            if (tid * f.rpt + i < m)
+                for (int l = 0; l < 2 * L; ++l) {
+                    const int o = f.off(i, tid) + l * f.LD;
+                    __pipeline_memcpy_async(sn + o, src + o, sizeof(double));
+                }
+        __pipeline_commit();
+        pref = true;
+    };
+
     // normalise column j (owner) and publish it; returns false on error
-    auto normalize_publish = [&](int j) -> bool {
-        double* col = colp(j);
+    auto normalize_publish = [&](int j, double* col) -> bool {
+        // chain mode: col is the chain's shared-memory copy; q_j also goes to
+        // the staging area (the next pivot's q) and to the published column
+        const bool copy_out = chain && col != colp(j);
+        double* pcol = colp(j);
         const bool tr = p.trace && tid == 0;
         R s = col_sq(col);
         if (tr) p.trace[j * 8 + 4] = gtimer();
@@ -225,6 +279,10 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
             code = stc;
         }
         if (tr) p.trace[j * 8 + 6] = gtimer();
+        // chain: the next pivot column, in flight during the divisions and
+        // the publish (tried here rather than after the norm tree: the bulk
+        // owner has had longer; measured 61 % ready at this point)
+        if (copy_out) chain_prefetch(j + 1);
         bool ok = (code == 0);
         if (ok) {
             for (int i = 0; i < f.rpt; ++i) {
@@ -233,6 +291,10 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
                     C qv = cdivide_real(a, rkk, rc);
                     if (!cfinite(qv)) ok = false;
                     f.store(col, i, tid, qv);
+                    if (copy_out) {
+                        f.store(pcol, i, tid, qv);
+                        f.store(smem, i, tid, qv);
+                    }
                 }
             }
         }
@@ -254,14 +316,115 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
         return ok;
     };
 
+    // remove_projection(q_k, a_j) (mgs.hpp:57-61) with q_k staged in smem;
+    // returns "all finite" (CTA-uniform)
+    auto update_col = [&](int j, int k, double* col) -> bool {
+        C r = cta_tree<LV, C>(m, f.rpt, red_c, [&](int i) {
+            return cmul(cconj(f.load(smem, i, tid)), f.load(col, i, tid));
+        });
+        // dev trace: the critical update's dot product done (second stamp block)
+        if (p.trace && tid == 0 && j == k + 1) p.trace[8 * (n + 1) + 8 * (k + 1)] = gtimer();
+        bool ok = cfinite(r);
+        for (int i = 0; i < f.rpt; ++i) {
+            if (tid * f.rpt + i < m) {
+                C a = f.load(col, i, tid);
+                a = csub(a, cmul(r, f.load(smem, i, tid)));
+                if (!cfinite(a)) ok = false;
+                f.store(col, i, tid, a);
+            }
+        }
+        ok = __syncthreads_and(ok);
+        if (tid == 0) {
+            if (!ok) record(1 + (long long)k * (ncol + 1) + (j - k), 0, XQR_OVERFLOW);
+            if (j < n)
+                store_aos<L>(rdst + ((int64_t)j * n + k) * L2, r);
+            else
+                store_aos<L>(ydst + (int64_t)k * L2, r);
+        }
+        return ok;
+    };
+
+    // two columns at once, per column exactly update_col's operations
+    auto update_pair = [&](int j1, int j2, int k) {
+        double* c1 = colp(j1);
+        double* c2 = colp(j2);
+        const cpair<C> rr = cta_tree<LV, cpair<C>>(m, f.rpt, red_p, [&](int i) {
+            const C qc = cconj(f.load(smem, i, tid));
+            return cpair<C>{cmul(qc, f.load(c1, i, tid)), cmul(qc, f.load(c2, i, tid))};
+        });
+        bool ok1 = cfinite(rr.x), ok2 = cfinite(rr.y);
+        for (int i = 0; i < f.rpt; ++i) {
+            if (tid * f.rpt + i < m) {
+                const C qi = f.load(smem, i, tid);
+                C a1 = f.load(c1, i, tid), a2 = f.load(c2, i, tid);
+                a1 = csub(a1, cmul(rr.x, qi));
+                a2 = csub(a2, cmul(rr.y, qi));
+                if (!cfinite(a1)) ok1 = false;
+                if (!cfinite(a2)) ok2 = false;
+                f.store(c1, i, tid, a1);
+                f.store(c2, i, tid, a2);
+            }
+        }
+        ok1 = __syncthreads_and(ok1);
+        ok2 = __syncthreads_and(ok2);
+        if (tid == 0) {
+            const long long pos_k = 1 + (long long)k * (ncol + 1);
+            if (!ok1) record(pos_k + (j1 - k), 0, XQR_OVERFLOW);
+            if (!ok2) record(pos_k + (j2 - k), 0, XQR_OVERFLOW);
+            store_aos<L>(rdst + ((int64_t)j1 * n + k) * L2, rr.x);
+            if (j2 < n)
+                store_aos<L>(rdst + ((int64_t)j2 * n + k) * L2, rr.y);
+            else
+                store_aos<L>(ydst + (int64_t)k * L2, rr.y);
+        }
+    };
+
     bool abort = pre_err;
-    if (!abort && c == 0) abort = !normalize_publish(0);
+    auto chain_load = [&](int j) {  // own rows of column j (published by its owner) -> sc
+        for (int i = 0; i < f.rpt; ++i)
+            if (tid * f.rpt + i < m) f.store(sc, i, tid, f.load_cg(colp(j), i, tid));
+    };
+    if (!abort && c == 0) {
+        if (chain) chain_load(0);
+        abort = !normalize_publish(0, chain ? sc : colp(0));
+    }
     if (pre_err && c == 0 && tid == 0) st_release(p.flags, 2);
 
+    if (chain && c == 0) {
+        // ---- the pivot chain: q_{j-1} staged in smem by this CTA's own
+        // normalisation; column j's earlier projections from its owner
+        for (int j = 1; j < n && !abort; ++j) {
+            // column j: prefetched into sn during the last pivot, or loaded now
+            if (pref) {
+                __pipeline_wait_prior(0);
+                double* t = sc;
+                sc = sn;
+                sn = t;
+            } else {
+                while (ld_acquire(p.cflags + j) < j - 1) __nanosleep(32);
+                chain_load(j);
+            }
+            if (p.trace && tid == 0) p.trace[j * 8 + 0] = gtimer();
+            const bool ok = update_col(j, j - 1, sc);
+            if (p.trace && tid == 0) p.trace[j * 8 + 1] = gtimer();
+            if (!ok) {
+                if (tid == 0) st_release(p.flags + j, 2);
+                abort = true;
+                break;
+            }
+            if (!normalize_publish(j, sc)) {
+                abort = true;
+                break;
+            }
+        }
+        __pipeline_wait_prior(0);  // nothing left in flight
+    }
+
     // ---- MGS rounds ----------------------------------------------------------------
-    for (int k = 0; k < n && !abort; ++k) {
-        // first owned column > k
-        int j0 = k + 1 + ((c - (k + 1)) % G + G) % G;
+    for (int k = 0; k < n && !abort && bulk; ++k) {
+        // first owned column > k (chain mode: the pivot column k+1 is the chain's)
+        int j0 = k + 1 + ((own0 - (k + 1)) % S + S) % S;
+        if (chain && j0 == k + 1 && j0 < n) j0 += S;
         if (j0 >= ncol) continue;
         // acquire q_k
         if (tid == 0) {
@@ -280,34 +443,25 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
         }
         __syncthreads();
         if (p.trace && tid == 0 && j0 == k + 1) p.trace[(k + 1) * 8 + 0] = gtimer();
-        const long long pos_k = 1 + (long long)k * (ncol + 1);
-        for (int j = j0; j < ncol; j += G) {
-            double* col = colp(j);
-            C r = cta_tree<LV, C>(m, f.rpt, red_c, [&](int i) {
-                return cmul(cconj(f.load(smem, i, tid)), f.load(col, i, tid));
-            });
-            // dev trace: the critical update's dot product done (second stamp block)
-            if (p.trace && tid == 0 && j == k + 1) p.trace[8 * (n + 1) + 8 * (k + 1)] = gtimer();
-            bool ok = cfinite(r);
-            for (int i = 0; i < f.rpt; ++i) {
-                if (tid * f.rpt + i < m) {
-                    C a = f.load(col, i, tid);
-                    a = csub(a, cmul(r, f.load(smem, i, tid)));
-                    if (!cfinite(a)) ok = false;
-                    f.store(col, i, tid, a);
+        for (int j = j0; j < ncol; j += S) {
+            // pairs, except the column the chain needs next (k+2): alone, and
+            // first, so its projection k is out as early as possible
+            if (chain && j != k + 2 && j + S < ncol) {
+                update_pair(j, j + S, k);
+                if (tid == 0) {
+                    st_release(p.cflags + j, k + 1);
+                    st_release(p.cflags + j + S, k + 1);
                 }
+                j += S;  // past the pair
+                continue;
             }
-            ok = __syncthreads_and(ok);
-            if (tid == 0) {
-                if (!ok) record(pos_k + (j - k), 0, XQR_OVERFLOW);
-                if (j < n)
-                    store_aos<L>(rdst + ((int64_t)j * n + k) * L2, r);
-                else
-                    store_aos<L>(ydst + (int64_t)k * L2, r);
-            }
+            const bool ok = update_col(j, k, colp(j));
+            // chain mode: column j has its first k+1 projections (an overflow
+            // still reports progress: the chain's normalisation records it)
+            if (chain && tid == 0) st_release(p.cflags + j, k + 1);
             if (p.trace && tid == 0 && j == k + 1) p.trace[(k + 1) * 8 + 1] = gtimer();
             if (ok && j == k + 1 && j < n) {
-                if (!normalize_publish(j)) {
+                if (!normalize_publish(j, colp(j))) {
                     abort = true;
                     break;
                 }
@@ -325,7 +479,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
     }
 
     // z = column_norm(b) by its owner (mgs.hpp:155)
-    if (LSQ && !abort && (n % G) == c) {
+    if (LSQ && !abort && bulk && (n % S) == own0) {
         R s = col_sq(colp(n));
         R z = rsqrt_ref(s);
         if (tid == 0) {
@@ -333,14 +487,16 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
             store_real<L>(p.z, 1, z);
         }
     }
+    if (!LSQ && chain) cg::this_grid().sync();  // the chain's published columns, visible to all
     if (!LSQ) {
-        // Q = the normalised owned columns: planar -> AoS
+        // Q = the normalised columns: planar -> AoS (L2 reads: in chain mode
+        // another CTA wrote them)
         for (int j = c; j < n; j += G) {
             const double* src = colp(j);
             double* dst = p.q + (int64_t)j * m * L2;
             for (int e = tid; e < m * L2; e += kGridThreads) {
                 const int plane = e % L2, i = e / L2;
-                dst[e] = src[plane * f.LD + f.row_off(i)];
+                dst[e] = __ldcg(src + plane * f.LD + f.row_off(i));
             }
         }
     }
@@ -378,8 +534,9 @@ template <int L, bool LSQ>
 cudaError_t launch_grid1(const GridParams& p, int grid, cudaStream_t s) {
     // rows per thread <= 4: a 3-level in-thread tree; 8 (m <= 2048): 4 levels
     auto kern = p.rpt <= 4 ? mgs_grid_kernel<L, 3, LSQ> : mgs_grid_kernel<L, 4, LSQ>;
-    const size_t smem = sizeof(double) * 2 * L * kGridThreads * p.rpt;
-    if (smem > 48 * 1024) {
+    // the q_k staging area, plus (chain mode) the chain's two pivot-column buffers
+    const size_t smem = sizeof(double) * 2 * L * kGridThreads * p.rpt * (p.chain ? 3 : 1);
+    {  // (static + dynamic may pass 48 KB even when the dynamic part does not)
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }

@@ -96,6 +96,8 @@ struct GridParams {
     int cs;                     // CTAs per cluster
     int* counters;              // [0] pre-pass arrivals, [1] final arrivals, [2] abort word
     int pair_bulk;              // xgrid2: update trailing columns two at a time (lockstep)
+    int chain;                  // xgrid1: CTA 0 runs every pivot (chain mode, xgrid1.cuh)
+    int* cflags;                // xgrid1 chain mode, ncol: projections applied per column
     int64_t sys;                // index written into the status (a batch solved system by system)
 };
 

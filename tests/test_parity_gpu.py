@@ -645,3 +645,19 @@ def test_grid_unplaceable_tall_system_fails_loudly(port, monkeypatch):
     monkeypatch.setenv("XQR_GRID_MAX_SMS", "0")
     with pytest.raises(xqr.cuda_error):
         xqr.lsq_solve(a, b)
+
+
+# ---- the grid kernels place every shape they are routed (no silent re-route) ------------
+@pytest.mark.parametrize("L,m,n", [(1, 256, 8), (2, 256, 8), (2, 300, 8), (2, 512, 8), (2, 1024, 6),
+                                   (2, 2048, 4), (4, 256, 8), (4, 512, 8), (4, 1024, 6), (4, 2048, 4)])
+def test_grid_shapes_place_without_reroute(port, L, m, n):
+    """Every row count the grid kernels serve launches on the full B200 (a
+    launch that fails for lack of shared memory would be re-routed to the
+    one-CTA kernel: the same bits, but tens of times slower -- only the
+    fallback counter shows it)."""
+    a, b = port.gen_system(L, m, n, 1.0, 9100 + m + n)
+    ctx = xqr.context(0)
+    before = ctx.grid_fallbacks
+    xqr.lsq_solve(a, b)
+    xqr.mgs_qr(a)
+    assert ctx.grid_fallbacks == before
