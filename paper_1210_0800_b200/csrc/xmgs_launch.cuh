@@ -41,6 +41,9 @@ static cudaError_t allow_dynamic_smem(K kern, size_t bytes, size_t& allowed) {
 template <int L, int LV, bool LSQ>
 static cudaError_t launch_one(const SolveParams& p, int rpl, cudaStream_t s) {
     constexpr int NW = cta_warps<L, LV>();
+#if XB_XSMEM
+    static_assert(NW * 32 <= XB_XS_THREADS, "the qd add's shared-memory slots (xarith.cuh) cover every thread");
+#endif
     auto kern = mgs_cta_kernel<mgs_warp<L, LV>, NW, LSQ, min_blocks<L, LV>()>;
     const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 32 * rpl);
     // static (the qd add's slots) + dynamic shared memory may exceed 48 KB
