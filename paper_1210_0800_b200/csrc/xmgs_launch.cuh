@@ -2,6 +2,7 @@
 // Each (limbs, mode) pair is instantiated in its own translation unit
 // (mgs_L*_*.cu) so the heavy quad-double kernels compile in parallel.
 #pragma once
+#include <atomic>
 #include "xmgs.cuh"
 
 namespace xb {
@@ -29,12 +30,20 @@ constexpr int min_blocks() {
 }
 
 // Opt a kernel in to `bytes` of dynamic shared memory; `allowed` (one per
-// kernel instance, kept by the caller) remembers the largest size granted.
+// kernel instance, kept by the caller) remembers the largest size granted
+// on each device (the attribute belongs to the device's context).
+constexpr int kMaxDevices = 64;
 template <class K>
-static cudaError_t allow_dynamic_smem(K kern, size_t bytes, size_t& allowed) {
-    if (bytes <= allowed) return cudaSuccess;
+static cudaError_t allow_dynamic_smem(K kern, size_t bytes, std::atomic<size_t>* allowed) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+    if (bytes <= allowed[dev].load(std::memory_order_relaxed)) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e == cudaSuccess) allowed = bytes;
+    if (e == cudaSuccess) {
+        size_t cur = allowed[dev].load(std::memory_order_relaxed);
+        while (cur < bytes && !allowed[dev].compare_exchange_weak(cur, bytes)) {
+        }
+    }
     return e;
 }
 
@@ -47,7 +56,7 @@ static cudaError_t launch_one(const SolveParams& p, int rpl, cudaStream_t s) {
     auto kern = mgs_cta_kernel<mgs_warp<L, LV>, NW, LSQ, min_blocks<L, LV>()>;
     const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 32 * rpl);
     // static (the qd add's slots) + dynamic shared memory may exceed 48 KB
-    static size_t allowed = 0;  // per template instance = per kernel
+    static std::atomic<size_t> allowed[kMaxDevices];  // per template instance = per kernel
     if (cudaError_t e = allow_dynamic_smem(kern, smem, allowed)) return e;
     kern<<<(unsigned)p.batch, NW * 32, smem, s>>>(p, rpl);
     return cudaGetLastError();
@@ -77,7 +86,7 @@ static cudaError_t launch_pair(const SolveParams& p, int rpp, cudaStream_t s) {
     auto kern = mgs_cta_kernel<mgs_pair<L>, NW, LSQ, XB_PAIR_MINB>;
     const size_t smem = 2 * sizeof(double) * (size_t)(2 * L * 16 * rpp);
     // static (the qd add's slots) + dynamic shared memory may exceed 48 KB
-    static size_t allowed = 0;  // per template instance = per kernel
+    static std::atomic<size_t> allowed[kMaxDevices];  // per template instance = per kernel
     if (cudaError_t e = allow_dynamic_smem(kern, smem, allowed)) return e;
     kern<<<(unsigned)p.batch, NW * 32, smem, s>>>(p, rpp);
     return cudaGetLastError();
