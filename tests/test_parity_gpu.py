@@ -661,3 +661,23 @@ def test_grid_shapes_place_without_reroute(port, L, m, n):
     xqr.lsq_solve(a, b)
     xqr.mgs_qr(a)
     assert ctx.grid_fallbacks == before
+
+
+# ---- both schedules of the double / double-double grid kernel --------------------------
+@pytest.mark.parametrize("chain", ["0", "1"])
+@pytest.mark.parametrize("L,m,n", [(2, 256, 40), (2, 300, 24), (1, 128, 64), (2, 64, 64)])
+def test_grid1_schedules_bitwise(port, monkeypatch, chain, L, m, n):
+    """The dd/d grid kernel's cyclic schedule and its chain mode (CTA 0 runs
+    every pivot, the other CTAs the earlier projections) give the reference's
+    bits for QR and least squares."""
+    monkeypatch.setenv("XQR_GRID_CHAIN", chain)
+    a, b = port.gen_system(L, m, n, 4.0, 5200 + m + n)
+    x, z, st = port.lsq_solve(a, b)
+    q, r, st2 = port.mgs_qr(a)
+    assert st[0] == 0 and st2[0] == 0
+    gx, gz = xqr.lsq_solve(a, b)
+    gq, gr = xqr.mgs_qr(a)
+    assert_same(gx, x, "x")
+    assert_same(gz, z, "z")
+    assert_same(gq, q, "q")
+    assert_same(gr, r, "r")
