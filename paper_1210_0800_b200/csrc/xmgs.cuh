@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) mgs_cta_kernel(SolveParams p, i
     __shared__ unsigned long long s_key;
     __shared__ int s_ctr[2];
     __shared__ R s_best[NW];
+    __shared__ double s_hmax[NW];
     __shared__ R s_thr;
     __shared__ R s_z;
 
@@ -169,14 +170,42 @@ __global__ void __launch_bounds__(NW * 32, MINB) mgs_cta_kernel(SolveParams p, i
     __syncthreads();
 
     // ---- norm pre-pass and breakdown threshold (mgs.hpp:91-96, :143) --------
+    // max_column_norm (mgs.hpp:72-80) = max_j sqrt(s_j), s_j = Re(a_j^H a_j).
+    // The square roots are taken only where they can decide the maximum:
+    // for the columns whose s_j is within a relative 2^-40 of the largest
+    // (compared on the head limbs) -- sqrt is monotone up to its rounding
+    // (double: exact; dd / qd: ~2^-104 / ~2^-208 relative, mgs.hpp / the
+    // reference's sqrt), so a column further down can never hold the
+    // largest norm, and the maximum of the rest is the reference's value
+    // bit for bit -- plus the extreme magnitudes, whose square roots could
+    // overflow on their own (the reference raises overflow_error there).
     bool err = false;
     {
+        double* sb = smem;  // s_j (L doubles each) in the pivot slots, free until pivot 0
+        double hmax = 0.0;
+        for (int j = warp; j < ncol; j += NW) {
+            const R s = W::col_sq(f, ws + (int64_t)j * f.COL, lane, m);
+            if (!vfinite(s)) err = true;
+            if (lane == 0) store_real<L>(sb + (int64_t)j * L, 1, s);
+            hmax = fmax(hmax, s.c0);
+        }
+        if (lane == 0) {
+            s_hmax[warp] = hmax;
+            if (err) atomicMin(&s_key, status_key(0, 0, XQR_OVERFLOW));
+        }
+        if (__syncthreads_or(err)) goto finish;
+        for (int w = 0; w < NW; ++w) hmax = fmax(hmax, s_hmax[w]);
+        const double near = hmax * (1.0 - 0x1p-40);
         R best = rmake<R>(0.0);
         for (int j = warp; j < ncol; j += NW) {
-            R s = W::col_sq(f, ws + (int64_t)j * f.COL, lane, m);
-            R nrm = rsqrt_ref(s);
-            if (!vfinite(s) || !vfinite(nrm)) err = true;
-            if (lt(best, nrm)) best = nrm;
+            R s;
+            load_real<L>(sb + (int64_t)j * L, 1, s);
+            const double h = s.c0;
+            if (h >= near || h > 0x1p1000 || (h != 0.0 && h < 0x1p-1000)) {
+                const R nrm = rsqrt_ref(s);
+                if (!vfinite(nrm)) err = true;
+                if (lt(best, nrm)) best = nrm;
+            }
         }
         if (lane == 0) {
             s_best[warp] = best;
