@@ -681,3 +681,36 @@ def test_grid1_schedules_bitwise(port, monkeypatch, chain, L, m, n):
     assert_same(gz, z, "z")
     assert_same(gq, q, "q")
     assert_same(gr, r, "r")
+
+
+# ---- the batched pre-pass's maximum column norm at the extremes ------------------------
+@pytest.mark.parametrize("L", [1, 2, 4])
+@pytest.mark.parametrize("scale", [505, 511, -500, -530, 0])
+def test_batched_prepass_extreme_and_tied_norms(port, L, scale):
+    """The batched kernels take square roots only for the columns that can
+    hold the largest norm (within 2^-40 of the largest s_j) and for extreme
+    magnitudes.  A batch mixing one column scaled by 2^scale (huge: near or
+    past overflow; tiny: below 2^-1000), exact duplicates of the largest
+    column (tied norms) and columns a last-limb step below it must give the
+    reference's results or error, system by system."""
+    rng = np.random.default_rng(6100 + L + scale)
+    m, n, batch = 48, 12, 4
+    A = np.stack([port.gen_system(L, m, n, 1.0, 300 + s)[0] for s in range(batch)])
+    B = np.stack([port.gen_system(L, m, n, 1.0, 300 + s)[1] for s in range(batch)])
+    A[0, 3] = A[0, 3] * 2.0 ** scale          # one extreme column
+    A[1, 5] = A[1, 2]                         # a tied (duplicate) column: breakdown
+    A[2, 7, :, :, -1] = np.nextafter(A[2, 7, :, :, -1], np.inf)  # last limbs nudged
+    A[2, 8] = A[2, 7]
+    A[2, 8, :, :, -1] = np.nextafter(A[2, 8, :, :, -1], -np.inf)
+    x, z, codes, cols = xqr.lsq_solve_batched(A, B)
+    for s in range(batch):
+        wx, wz, st = port.lsq_solve(A[s], B[s])
+        assert codes[s] == st[0], f"system {s}: code {codes[s]} vs {st[0]}"
+        if st[0] == 1:
+            assert cols[s] == st[1], f"system {s}"
+        if st[0] == 0:
+            if L == 1:
+                assert_same_nan(x[s], wx, f"x[{s}]")
+            else:
+                assert_same(x[s], wx, f"x[{s}]")
+                assert_same(z[s], wz, f"z[{s}]")
