@@ -218,7 +218,8 @@ def single_system_latency(xqr, ctx, torch, limbs, m, n, reps=20, warm=3, cpu=Non
     """One single-system config (configs[1..3]): device-resident latency (the
     device-pointer entry point; median of `reps` launches after `warm`
     warm-ups, CUDA events on the ctx stream per launch), the host-buffer
-    xqr_lsq_solve latency (numpy in, numpy out: H2D, solve, D2H; median),
+    xqr_lsq_solve latency (pinned numpy in, numpy out: H2D, solve, D2H;
+    median; also with pageable inputs),
     bitwise check against the reference's golden x, z, and -- with `cpu`
     (the reference build) -- the reference's lsq_solve on one host core and
     its par_lsq_solve on every core (parallel.hpp:105-153), timed once."""
@@ -249,16 +250,26 @@ def single_system_latency(xqr, ctx, torch, limbs, m, n, reps=20, warm=3, cpu=Non
         g = np.load(golden)
         parity = bool(np.array_equal(dx.cpu().numpy()[0].view(np.uint64), g["x"].view(np.uint64))
                       and np.array_equal(dz.cpu().numpy()[0].view(np.uint64), g["z"].view(np.uint64)))
-    # end to end through the host-buffer public API (xqr_lsq_solve)
+    # end to end through the host-buffer public API (xqr_lsq_solve): inputs
+    # in pinned host memory (as the batched e2e), x and z back into numpy
+    pa = torch.from_numpy(a[0]).pin_memory().numpy()
+    pb = torch.from_numpy(b[0]).pin_memory().numpy()
     for _ in range(warm):
-        xqr.lsq_solve(a[0], b[0])
+        xqr.lsq_solve(pa, pb)
     e2e = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        hx, hz = xqr.lsq_solve(a[0], b[0])
+        hx, hz = xqr.lsq_solve(pa, pb)
         e2e.append(time.perf_counter() - t0)
+    # the same call with pageable numpy inputs (the driver stages them)
+    e2e_pg = []
+    for _ in range(max(3, reps // 4)):
+        t0 = time.perf_counter()
+        xqr.lsq_solve(a[0], b[0])
+        e2e_pg.append(time.perf_counter() - t0)
     out = {"us_per_system": ms * 1e3, "us_min": times[0] * 1e3, "us_max": times[-1] * 1e3, "reps": reps,
            "e2e_us": float(np.median(e2e)) * 1e6,
+           "e2e_us_pageable_inputs": float(np.median(e2e_pg)) * 1e6,
            "fp64_gflops": flops / (ms * 1e-3) / 1e9,
            "bitwise_vs_reference": parity,
            "e2e_matches_device": bool(np.array_equal(hx.view(np.uint64), dx.cpu().numpy()[0].view(np.uint64)))}
