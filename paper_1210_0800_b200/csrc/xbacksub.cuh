@@ -13,15 +13,62 @@
 
 namespace xb {
 
+// Quad-double t with every limb zero -- always so for MGS, whose diagonal is
+// real: t = 0 / r_kk.  Then mul(x, t) (quad_double.hpp:267-338) is a
+// function of the SIGN BITS of x alone for finite x: every partial product is
+// a zero whose sign is the XOR of its factors' signs, every fma error term
+// (x_i t_j) + (-p) is +0, and everything after adds and renormalises zeros.
+// The 16 possible results (a sign nibble each) are computed once per pivot,
+// off the sequential sweep, by mul itself on one representative per sign
+// pattern, and the sweep then looks its product up instead of running a qd
+// multiply whose renormalisation takes the reference's all-zero branch path.
+XB_DEVICE int sign_nibble(const r4& x) {
+    return (dbits(x.c0) < 0 ? 1 : 0) | (dbits(x.c1) < 0 ? 2 : 0) | (dbits(x.c2) < 0 ? 4 : 0) |
+           (dbits(x.c3) < 0 ? 8 : 0);
+}
+XB_DEVICE r4 zeros_signed(int nib) {
+    return {(nib & 1) ? -0.0 : 0.0, (nib & 2) ? -0.0 : 0.0, (nib & 4) ? -0.0 : 0.0, (nib & 8) ? -0.0 : 0.0};
+}
+XB_DEVICE bool all_zero(const r4& x) { return x.c0 == 0.0 && x.c1 == 0.0 && x.c2 == 0.0 && x.c3 == 0.0; }
+XB_DEVICE bool all_finite(const r4& x) { return finite(x.c0) && finite(x.c1) && finite(x.c2) && finite(x.c3); }
+// the table: nibble of mul(rep(pattern), t) at bits 4*pattern; ok = false if
+// some product is not all zeros (then the table is not used)
+XB_DEVICE unsigned long long zero_mul_table(const r4& t, bool& ok) {
+    unsigned long long mask = 0;
+    ok = true;
+#pragma unroll 1
+    for (int pat = 0; pat < 16; ++pat) {
+        const r4 rep{(pat & 1) ? -1.0 : 1.0, (pat & 2) ? -0x1p-60 : 0x1p-60, (pat & 4) ? -0x1p-120 : 0x1p-120,
+                     (pat & 8) ? -0x1p-180 : 0x1p-180};
+        const r4 z = mul(rep, t);
+        ok = ok && all_zero(z);
+        mask |= (unsigned long long)sign_nibble(z) << (4 * pat);
+    }
+    return mask;
+}
+
 template <int L>
 struct smith_prep {
     real_t<L> t, d;
     recip_t<real_t<L>> rc;
     int br;    // abs(d.re) >= abs(d.im)
     int code;  // error the division of x_k raises in the reference (0 = none)
+    int zt = 0;                   // quad-double: t is all zeros, products from ztab
+    unsigned long long ztab = 0;  // (zero_mul_table)
 };
+// mul(x, s.t) for the Smith numerator (complex.hpp:53/56), by the table when
+// it applies (finite x; otherwise the multiply itself)
+template <int L>
+XB_DEVICE real_t<L> smith_tmul(const real_t<L>& x, const smith_prep<L>& s) {
+    if constexpr (L == 4) {
+        if (s.zt && all_finite(x)) return zeros_signed((int)(s.ztab >> (4 * sign_nibble(x))) & 15);
+    }
+    return mul(x, s.t);
+}
 
-// Store/load the prep record (3L+1 doubles) in global scratch.
+// Store/load the prep record (3L+1 doubles) in global scratch.  Quad-double
+// with zt: the table's 64 bits take t's head slot, t's sign bits go with the
+// flags (t itself is zeros).
 template <int L>
 XB_DEVICE void prep_store(double* p, const smith_prep<L>& s) {
     store_real<L>(p, 1, s.t);
@@ -29,7 +76,14 @@ XB_DEVICE void prep_store(double* p, const smith_prep<L>& s) {
     if constexpr (L == 1) p[2] = s.rc.b;
     if constexpr (L == 2) store_real<2>(p + 2 * L, 1, s.rc.x1);
     if constexpr (L == 4) store_real<4>(p + 2 * L, 1, s.rc.x);
-    p[3 * L] = (double)(s.br | (s.code << 4));
+    int flags = s.br | (s.code << 4);
+    if constexpr (L == 4) {
+        if (s.zt) {
+            flags |= (1 << 8) | (sign_nibble(s.t) << 9);
+            p[0] = __longlong_as_double((long long)s.ztab);
+        }
+    }
+    p[3 * L] = (double)flags;
 }
 template <int L>
 XB_DEVICE smith_prep<L> prep_load(const double* p) {
@@ -41,7 +95,14 @@ XB_DEVICE smith_prep<L> prep_load(const double* p) {
     if constexpr (L == 4) load_real<4>(p + 2 * L, 1, s.rc.x);
     int f = (int)p[3 * L];
     s.br = f & 15;
-    s.code = f >> 4;
+    s.code = (f >> 4) & 15;
+    if constexpr (L == 4) {
+        s.zt = (f >> 8) & 1;
+        if (s.zt) {
+            s.ztab = (unsigned long long)__double_as_longlong(p[0]);
+            s.t = zeros_signed((f >> 9) & 15);
+        }
+    }
     return s;
 }
 
@@ -62,7 +123,16 @@ XB_DEVICE void store_aos(double* p, const cx<real_t<L>>& z) {
 template <int L>
 XB_DEVICE cx<real_t<L>> smith_apply(const cx<real_t<L>>& a, const smith_prep<L>& s) {
     using R = real_t<L>;
-    rpair<R> p = mul2(a.im, s.t, a.re, s.t);
+    rpair<R> p;
+    if constexpr (L == 4) {
+        if (s.zt) {
+            p = {smith_tmul<L>(a.im, s), smith_tmul<L>(a.re, s)};
+        } else {
+            p = mul2(a.im, s.t, a.re, s.t);
+        }
+    } else {
+        p = mul2(a.im, s.t, a.re, s.t);
+    }
     rpair<R> nu = s.br ? add2(a.re, p.x, a.im, neg(p.y))    // a.re + a.im*t, a.im - a.re*t
                        : add2(p.y, a.im, p.x, neg(a.re));  // a.re*t + a.im, a.im*t - a.re
     return cdivide_real(cx<R>{nu.x, nu.y}, s.d, s.rc);
@@ -102,6 +172,13 @@ XB_DEVICE void cta_backsub_prep(int n, const double* r, const double* y, double*
             }
             if (!dst && (!vfinite(s.t) || !vfinite(s.d))) dst = 2;
             if (!dst) s.rc = recip(s.d, dst);
+            if constexpr (L == 4) {
+                if (!dst && all_zero(s.t)) {
+                    bool ok = false;
+                    s.ztab = zero_mul_table(s.t, ok);
+                    s.zt = ok ? 1 : 0;
+                }
+            }
         }
         s.code = dst;
         prep_store<L>(prep + (size_t)k * (3 * L + 1), s);
@@ -269,10 +346,10 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
         code = sp.code;
         R num;
         if (sp.br) {
-            const R prod = mul(part ? are : aim, sp.t);
+            const R prod = smith_tmul<L>(part ? are : aim, sp);
             num = add(part ? aim : are, part ? neg(prod) : prod);
         } else {
-            const R prod = mul(part ? aim : are, sp.t);
+            const R prod = smith_tmul<L>(part ? aim : are, sp);
             num = add(prod, part ? neg(are) : aim);
         }
         return divide_inline(num, sp.d, sp.rc);
