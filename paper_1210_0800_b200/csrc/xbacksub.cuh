@@ -56,6 +56,18 @@ struct smith_prep {
     int zt = 0;                   // quad-double: t is all zeros, products from ztab
     unsigned long long ztab = 0;  // (zero_mul_table)
 };
+// x + z (either operand order) with z a qd of zeros equals x bit for bit
+// when x is canonical: four non-zero finite limbs with fl(x_i + x_{i+1}) =
+// x_i.  Walking the reference merge (quad_double.hpp:216-257): x's limbs
+// come first (|x_i| > 0), each two_sum of adjacent limbs returns them
+// unchanged, the two steps on x_2, x_3 emit x_0, x_1, the four steps on the
+// zeros emit nothing (their error term is +0 whatever the zero's sign), the
+// loop exit writes x_2, x_3, and renorm4 of a canonical tuple is the tuple.
+XB_DEVICE bool qd_canonical(const r4& x) {
+    return x.c0 != 0.0 && x.c1 != 0.0 && x.c2 != 0.0 && x.c3 != 0.0 && all_finite(x) &&
+           dadd(x.c0, x.c1) == x.c0 && dadd(x.c1, x.c2) == x.c1 && dadd(x.c2, x.c3) == x.c2;
+}
+
 // mul(x, s.t) for the Smith numerator (complex.hpp:53/56), by the table when
 // it applies (finite x; otherwise the multiply itself)
 template <int L>
@@ -345,12 +357,19 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
         const smith_prep<L> sp = prep_load<L>(prep + (size_t)j * (3 * L + 1));
         code = sp.code;
         R num;
+        // (a zero product added to a canonical x leaves x: qd_canonical)
         if (sp.br) {
+            const R x = part ? aim : are;
             const R prod = smith_tmul<L>(part ? are : aim, sp);
-            num = add(part ? aim : are, part ? neg(prod) : prod);
+            bool keep = false;
+            if constexpr (L == 4) keep = sp.zt && all_zero(prod) && qd_canonical(x);
+            num = keep ? x : add(x, part ? neg(prod) : prod);
         } else {
+            const R x = part ? neg(are) : aim;
             const R prod = smith_tmul<L>(part ? aim : are, sp);
-            num = add(prod, part ? neg(are) : aim);
+            bool keep = false;
+            if constexpr (L == 4) keep = sp.zt && all_zero(prod) && qd_canonical(x);
+            num = keep ? x : add(prod, x);
         }
         return divide_inline(num, sp.d, sp.rc);
     };
