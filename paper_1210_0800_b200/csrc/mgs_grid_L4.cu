@@ -5,6 +5,7 @@
 
 namespace xb {
 cudaError_t launch_grid_L4_wide(const GridParams& p, int max_clusters, bool lsq, cudaStream_t s);
+cudaError_t launch_grid_L4_backsub(const GridParams& p, cudaStream_t s);
 
 cudaError_t launch_grid_L4(const GridParams& p, int max_clusters, bool lsq, cudaStream_t s) {
     cudaError_t e;
@@ -15,6 +16,6 @@ cudaError_t launch_grid_L4(const GridParams& p, int max_clusters, bool lsq, cuda
         default: return cudaErrorInvalidValue;
     }
     if (e != cudaSuccess || !lsq) return e;
-    return launch_grid2_backsub<4>(p, s);
+    return launch_grid_L4_backsub(p, s);
 }
 }  // namespace xb

@@ -307,8 +307,23 @@ XB_DEVICE bool cta_back_substitute(int n, const double* r, const double* y, doub
 // are shared memory; blockDim.x is a multiple of 32, at least 64.  Returns
 // (uniformly) true on error.
 #ifndef XB_BS_ISOLATE
-#define XB_BS_ISOLATE 1
+#define XB_BS_ISOLATE 2
 #endif
+// CTA-scope flag handoff in shared memory: an acquire load is a plain LDS on
+// sm_100a (no fence); a release store costs one MEMBAR.ALL.CTA, lighter than
+// the MEMBAR.SC.CTA that __threadfence_block() emits
+XB_DEVICE int bs_acquire(const volatile int* f) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];"
+                 : "=r"(v)
+                 : "r"((unsigned)__cvta_generic_to_shared((const void*)f))
+                 : "memory");
+    return v;
+}
+XB_DEVICE void bs_release(volatile int* f, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared((void*)f)), "r"(v)
+                 : "memory");
+}
 template <int L>
 XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, double* xs, double* prep,
                                     int* sync, unsigned long long* key, long long pos_base,
@@ -319,7 +334,15 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
     // XB_BS_ISOLATE: the warps sharing the finisher's SM sub-partition (warp
     // id = 0 mod 4) stay idle, so the sequential chain does not compete for
     // that SMSP's FP64 issue; updater u runs on warp u + 1 + u / 3
-#if XB_BS_ISOLATE
+#if XB_BS_ISOLATE == 2
+    // ... until every other warp holds a block: the idle ones then take the
+    // next slots (16 * (NW - 1) unknowns per sweep)
+    const int NR = NW - (NW + 3) / 4;  // updaters off the finisher's SMSP
+    const int NU = NW - 1;
+    const bool updater = warp > 0;
+    const int uo = (warp & 3) ? warp - 1 - (warp >> 2) : NR + (warp >> 2) - 1;
+    auto uwarp = [NR](int u) { return u < NR ? u + 1 + u / 3 : 4 * (u - NR + 1); };
+#elif XB_BS_ISOLATE
     const int NU = NW - (NW + 3) / 4;
     const bool updater = warp > 0 && (warp & 3) != 0;
     const int uo = warp - 1 - (warp >> 2);
@@ -334,7 +357,9 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
     const unsigned pmask = 3u << (lane & 30);
     volatile int* frontier = sync;  // lowest k whose x_k is final and in xs
     volatile int* stop = sync + 1;  // highest step at which an error occurred
-    volatile int* done = sync + 2;  // done[w]: updater w applied every x_k, k >= done[w]
+    // hi[w]: updater w applied every x_k, k > hi[w], to all its unknowns and
+    // x_{hi[w]} to its highest block (which holds the finisher's next unknown)
+    volatile int* hi = sync + 2;
     cta_backsub_prep<L>(n, r, y, xs, prep);
     if (tid == 0) {
         sync[0] = n;
@@ -401,16 +426,21 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
             store_real<L>(xs_part(n - 1, part), 1, v);
             __syncwarp(3u);
             if (lane == 0) {
-                __threadfence_block();
-                *frontier = n - 1;
+                bs_release(frontier, n - 1);
             }
+            // owner (updater index) of x_{k-1}, stepped down with k: no division on the chain
+            int ublk = n >= 2 ? ((n - 2) >> 4) % NU : 0;
             for (int k = n - 1; k >= 1 && !err; --k) {
                 // dev instrumentation (XQR_GRID_TRACE): SM cycles per phase
                 unsigned long long c0 = trace ? clock64() : 0;
                 // x_{k-1} has every update but x_k's once its updater is past k+1
-                const int w = uwarp(((k - 1) >> 4) % NU);
-                while (done[w] > k + 1 && *stop < k) __nanosleep(20);
-                __threadfence_block();
+                const int w = uwarp(ublk);
+                if (((k - 1) & 15) == 0) ublk = ublk ? ublk - 1 : NU - 1;
+                int spins = 0;
+                while (bs_acquire(&hi[w]) > k + 1 && bs_acquire(stop) < k) {
+                    __nanosleep(20);
+                    ++spins;
+                }
                 unsigned long long c1 = trace ? clock64() : 0, c2 = 0;
                 if (*stop >= k) break;
                 // (y1, y2) = (own half, other half) of x_k
@@ -439,8 +469,7 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
                 store_real<L>(xs_part(k - 1, part), 1, v);
                 __syncwarp(3u);
                 if (lane == 0) {
-                    __threadfence_block();
-                    *frontier = k - 1;
+                    bs_release(frontier, k - 1);
                 }
                 if (trace && lane == 0) {
                     trace[8 * k + 0] = c0;
@@ -448,6 +477,7 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
                     trace[8 * k + 2] = c2;
                     trace[8 * k + 3] = c3;
                     trace[8 * k + 4] = clock64();
+                    trace[8 * k + 7] = spins;
                 }
             }
         }
@@ -457,20 +487,23 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
         int k = n - 1;
         for (; k >= 2; --k) {
             if (16 * uo > k - 2) break;  // every own unknown is past its updates
-            if (lane == 0)
-                while (*frontier > k && *stop < k) __nanosleep(32);
-            __syncwarp();
-            __threadfence_block();
+            if (lane == 0) {
+                while (bs_acquire(frontier) > k && bs_acquire(stop) < k) __nanosleep(32);
+            }
+            __syncwarp();  // orders lane 0's acquire before the warp's reads
             if (__any_sync(kFull, *stop >= k)) break;
+            // dev instrumentation: the finisher's next input (x_{k-2}) taken / done
+            const bool crit = trace && lane == 0 && uwarp(((k - 2) >> 4) % NU) == warp;
+            if (crit) trace[8 * (k - 1) + 5] = clock64();
             R xkre, xkim;
             load_real<L>(xs_part(k, 0), 1, xkre);
             load_real<L>(xs_part(k, 1), 1, xkim);
             const R y1 = part ? xkim : xkre, y2 = part ? xkre : xkim;
-            // highest own j <= k-2 first: the finisher needs x_{k-2} next
-            for (int j = base <= k - 2 ? base + ((k - 2 - base) / BW) * BW : -1; j >= 0; j -= BW) {
-#ifdef XB_BS_EXPERIMENT
-                continue;
-#endif
+            // highest own j <= k-2 first: the finisher needs x_{k-2} next --
+            // and may take it as soon as this warp's highest block is done
+            // (`hi`), before the lower blocks
+            const int j0 = base <= k - 2 ? base + ((k - 2 - base) / BW) * BW : -1;
+            auto upd = [&](int j) {
                 R rre, rim, xj;
                 load_real<L>(rpart(j, k, 0), 1, rre);
                 load_real<L>(rpart(j, k, 1), 1, rim);
@@ -478,19 +511,23 @@ XB_DEVICE bool flow_back_substitute(int n, const double* r, const double* y, dou
                 const R v = update(xj, rre, rim, y1, y2);
                 if (!vfinite(v) || !vfinite(shfl_pair(v, pmask))) fail(k, 2);
                 store_real<L>(xs_part(j, part), 1, v);
-            }
+            };
+#ifndef XB_BS_EXPERIMENT
+            if (j0 >= 0) upd(j0);
             __syncwarp();
             if (lane == 0) {
-                __threadfence_block();
-                done[warp] = k;
+                bs_release(&hi[warp], k);
+                if (crit) trace[8 * (k - 1) + 6] = clock64();
             }
+            for (int j = j0 - BW; j >= 0; j -= BW) upd(j);
+#endif
             // R is known from the start: pull next step's r_{j,k-1} into L1
             for (int j = base <= k - 3 ? base + ((k - 3 - base) / BW) * BW : -1; j >= 0; j -= BW)
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(rpart(j, k - 1, part)));
         }
         __syncwarp();
-        if (lane == 0 && k < 2) done[warp] = -1;  // nothing left: never hold the finisher
-        if (lane == 0 && k >= 2 && 16 * uo > k - 2) done[warp] = -1;
+        if (lane == 0 && k < 2) hi[warp] = -1;  // nothing left: never hold the finisher
+        if (lane == 0 && k >= 2 && 16 * uo > k - 2) hi[warp] = -1;
     }
     return __syncthreads_or(err);
 }

@@ -594,10 +594,14 @@ __global__ void __launch_bounds__(kG2Threads, 2) mgs_grid2_kernel(GridParams p) 
 // :110-126): one CTA of kG2BsThreads threads, one lane pair per unknown for
 // n <= 256 warp-specialised (flow_back_substitute): a finisher warp runs the
 // chain, updater warps trail it; no CTA barrier per step.
-constexpr int kG2BsThreads = 512;
+#ifndef XB_G2BS_THREADS
+#define XB_G2BS_THREADS 512
+#endif
+constexpr int kG2BsThreads = XB_G2BS_THREADS;
 template <int L>
 __host__ __device__ constexpr bool g2_backsub_prep_in_smem(int n) {
-    return sizeof(double) * (size_t)n * (2 * L + 3 * L + 1) <= 200 * 1024;
+    // 227 KB less the static merge slots (XB_XSMEM) and the flags
+    return sizeof(double) * (size_t)n * (2 * L + 3 * L + 1) <= 227 * 1024 - 64 * XB_XS_THREADS - 1024;
 }
 template <int L>
 __host__ __device__ constexpr size_t g2_backsub_smem(int n) {

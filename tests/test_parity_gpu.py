@@ -299,7 +299,7 @@ def test_back_substitute_flow(port, L):
     an overflowing update above a zero diagonal (the overflow comes first in
     program order, mgs.hpp:117-124) and the other way round."""
     rng = np.random.default_rng(100 + L)
-    for n in (16, 17, 255, 256, 257, 300, 513):
+    for n in (16, 17, 193, 241, 255, 256, 257, 300, 513):
         r, y = _upper(rng, n, L)
         x, st = port.back_substitute(r, y)
         assert st == (0, 0)

@@ -84,12 +84,30 @@ def main():
                 avg = rows[lo:hi].mean(axis=0)
                 print(f"  pivots {lo + 2}-{hi + 1}: " + ", ".join(f"{k} {v:.1f}" for k, v in zip(names, avg)) + " us")
         if args.phases:
+            n_rows = t.shape[0] - 1
             c = t[1:-1, 9:14].astype(np.int64)  # back-substitution steps k = 1 .. n-1 (SM cycles)
             c = c[c[:, 0] != 0]
             ph = np.diff(c, axis=1).mean(axis=0)
             loop = (c[:-1, 0] - c[1:, 4]).mean() if len(c) > 1 else 0
             print(f"  finisher cycles/step: wait {ph[0]:.0f}, update {ph[1]:.0f}, smith {ph[2]:.0f}, "
                   f"publish {ph[3]:.0f}, loop {loop:.0f}")
+            # updater of the finisher's next input: row k-1 slots 5/6 = x_k taken / x_{k-2} updated;
+            # x_k published at the end of step k+1 (row k+1 slot 3)
+            B = t[:, 9:16].astype(np.int64)
+            u = [(B[k - 1, 5] - B[k + 1, 3], B[k - 1, 6] - B[k - 1, 5], B[k - 1, 0] - B[k - 1, 6])
+                 for k in range(3, n_rows - 1) if B[k - 1, 5] and B[k - 1, 6] and B[k + 1, 3] and B[k - 1, 0]]
+            sp = t[2:-1, 16].astype(np.int64)
+            W = (t[2:-1, 10].astype(np.int64) - t[2:-1, 9].astype(np.int64))
+            ks = np.arange(2, n_rows)
+            for lo in range(0, n_rows, 32):
+                sel = (ks >= lo) & (ks < lo + 32) & (t[2:-1, 9] != 0)
+                if sel.any():
+                    print(f"    steps {lo}-{lo + 31}: wait {W[sel].mean():.0f} cycles, "
+                          f"waiting {(sp[sel] > 0).mean() * 100:.0f} %, spins {sp[sel].mean():.1f}")
+            if u:
+                u = np.array(u, dtype=np.float64).mean(axis=0)
+                print(f"  next-input updater cycles: poll {u[0]:.0f}, update {u[1]:.0f}, "
+                      f"slack to the finisher {u[2]:.0f}")
         print(f"rep {rep}: factorisation {fact:.1f} us, gap {(bs_start - grid_end) / 1e3:.1f} us, "
               f"back substitution {(bs_end - bs_start) / 1e3:.1f} us", flush=True)
 
