@@ -252,6 +252,41 @@ XB_DEVICE bool cta_back_substitute(int n, const double* r, const double* y, doub
         store_aos<L>(xs + (size_t)(n - 1) * 2 * L, xk);
     }
     if (__syncthreads_or(err)) return true;
+    if (n <= nt) {
+        // one unknown per thread: x_j stays in registers and r_{j,k-1} is
+        // read ahead during step k, so the step is the arithmetic + a barrier
+        const int j = tid;
+        C xj{}, rn{};
+        if (j < n) xj = load_aos<L>(xs + (size_t)j * 2 * L);
+        if (j < n - 1) rn = load_aos<L>(r + ((size_t)(n - 1) * n + j) * 2 * L);
+        for (int k = n - 1; k >= 1; --k) {
+            const C xk = load_aos<L>(xs + (size_t)k * 2 * L);
+            const C rc = rn;
+            if (j < k - 1) rn = load_aos<L>(r + ((size_t)(k - 1) * n + j) * 2 * L);
+            if (j < k) {
+                xj = csub(xj, cmul(rc, xk));
+                if (!cfinite(xj)) {
+                    atomicMin(key, status_key(pos_base + (n - 1 - k), 0, 2));
+                    err = true;
+                } else if (j == k - 1) {
+                    smith_prep<L> s = prep_load<L>(prep + (size_t)j * (3 * L + 1));
+                    if (s.code) {
+                        atomicMin(key, status_key(pos_base + (n - k), 0, s.code));
+                        err = true;
+                    } else {
+                        xj = smith_apply<L>(xj, s);
+                        if (!cfinite(xj)) {
+                            atomicMin(key, status_key(pos_base + (n - k), 0, 2));
+                            err = true;
+                        }
+                    }
+                }
+                if (j == k - 1) store_aos<L>(xs + (size_t)j * 2 * L, xj);  // final: the next steps read it
+            }
+            if (__syncthreads_or(err)) return true;
+        }
+        return false;
+    }
     for (int k = n - 1; k >= 1; --k) {
         const C xk = load_aos<L>(xs + (size_t)k * 2 * L);
         const double* rk = r + (size_t)k * n * 2 * L;
@@ -294,8 +329,10 @@ XB_DEVICE bool cta_back_substitute(int n, const double* r, const double* y, doub
 //     publishes it (shared memory + a monotone `frontier`);
 //   * warps 1..NW-1 are UPDATERS: unknowns are dealt to them in blocks of 16
 //     (one per lane pair); for every published x_k, in order, an updater
-//     applies x_j -= r_jk x_k to its own j <= k-2 and then advances its
-//     `done` mark, which is what the finisher waits for before taking x_{k-1}.
+//     applies x_j -= r_jk x_k to its own j <= k-2, highest block first, and
+//     advances its `hi` mark after that block -- what the finisher waits for
+//     before taking x_{k-1}.  Slots past the other warps' go to the warps on
+//     the finisher's SMSP (XB_BS_ISOLATE 2), which stay idle for n <= 16 NR.
 // Nothing on the chain waits for a CTA barrier or for another pair's
 // data-dependent (divergent) add paths; R is read ahead into registers.
 //

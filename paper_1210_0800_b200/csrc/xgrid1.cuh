@@ -148,6 +148,8 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
 
     double* rdst = LSQ ? p.rws : p.r;
     double* ydst = LSQ ? p.rws + (int64_t)n * n * L2 : nullptr;
+    // dev trace, row n: 7 start, 4 factorised, 5/6 back substitution span
+    if (p.trace && c == 0 && tid == 0) p.trace[n * 8 + 7] = gtimer();
     auto colp = [&](int j) { return p.ws + (int64_t)j * f.COL; };
     // Column ownership.  Cyclic mode: column j -> CTA j mod G, whose owner of
     // column k+1 updates it first in round k and normalises it.  Chain mode
@@ -505,6 +507,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
     if (c == 0) {
         __shared__ unsigned long long s_key;
         if (tid == 0) s_key = __ldcg(p.key);
+        if (p.trace && tid == 0) p.trace[n * 8 + 4] = p.trace[n * 8 + 5] = gtimer();
         __syncthreads();
         if (LSQ && s_key == kNoError) {
             // fused back substitution (mgs.hpp:157 -> :110-126); x in smem
@@ -514,6 +517,7 @@ __global__ void __launch_bounds__(kGridThreads, 1) mgs_grid_kernel(GridParams p)
             if (!bad)
                 for (int e = tid; e < n * L2; e += kGridThreads) p.x[e] = smem[e];
             __syncthreads();
+            if (p.trace && tid == 0) p.trace[n * 8 + 6] = gtimer();
         }
         if (tid == 0) {
             unsigned long long key = s_key;

@@ -304,8 +304,9 @@ def test_back_substitute_flow(port, L):
         x, st = port.back_substitute(r, y)
         assert st == (0, 0)
         assert_same(xqr.back_substitute(r, y), x, f"n={n}")
-    n = 300
-    for k_over, k_zero in ((250, 100), (40, 200), (299, 17), (5, 6)):
+    # n = 300: several unknowns per thread; n = 200: the one-per-thread sweep
+    for n, k_over, k_zero in ((300, 250, 100), (300, 40, 200), (300, 299, 17), (300, 5, 6),
+                              (200, 150, 60), (200, 30, 120), (200, 199, 1)):
         r, y = _upper(rng, n, L)
         r[k_over, : k_over, :, 0] = 1e300  # x_j -= r_jk x_k overflows at step k_over
         y[k_over, :, 0] = 1e300
