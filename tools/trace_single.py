@@ -75,11 +75,12 @@ def main():
                 for j in range(2, n - 1):
                     cur = T[j]
                     tt = int(t[j, 16])
-                    if min(cur[0], cur[1], cur[3], tt) == 0:
-                        continue
+                    if min(cur[0], cur[1], cur[3], tt) == 0 or not cur[0] <= tt <= cur[1]:
+                        continue  # (no tree stamp in this build: the slot holds back-substitution data)
                     sp.append([cur[3] - cur[0], tt - cur[3], cur[1] - tt])
-                sp = np.array(sp, dtype=np.float64) / 1e3
-                print("  update split (us): leaf %.1f, tree %.1f, axpy+sync %.1f" % tuple(sp.mean(axis=0)))
+                if sp:
+                    sp = np.array(sp, dtype=np.float64) / 1e3
+                    print("  update split (us): leaf %.1f, tree %.1f, axpy+sync %.1f" % tuple(sp.mean(axis=0)))
             for lo, hi in ((0, len(rows) // 3), (len(rows) // 3, 2 * len(rows) // 3), (2 * len(rows) // 3, len(rows))):
                 avg = rows[lo:hi].mean(axis=0)
                 print(f"  pivots {lo + 2}-{hi + 1}: " + ", ".join(f"{k} {v:.1f}" for k, v in zip(names, avg)) + " us")
