@@ -715,3 +715,24 @@ def test_batched_prepass_extreme_and_tied_norms(port, L, scale):
             else:
                 assert_same(x[s], wx, f"x[{s}]")
                 assert_same(z[s], wz, f"z[{s}]")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(200, 200), (240, 230)])
+def test_batched_qd_back_substitution_many_blocks(port, m, n):
+    """The batched quad-double kernels' warp-specialised back substitution
+    with more unknowns than one sweep of the updaters off the finisher's
+    SMSP (16 per warp), so the warps on the finisher's SMSP take the next
+    blocks and some updaters carry two: each system bitwise equal to the
+    single-system solve of the same data (itself pinned to the oracle)."""
+    batch = 2
+    a = np.zeros((batch, n, m, 2, 4))
+    b = np.zeros((batch, m, 2, 4))
+    for s in range(batch):
+        a[s], b[s] = port.gen_system(4, m, n, 1.0, 77, s)
+    x, z, codes, cols = xqr.lsq_solve_batched(a, b)
+    for s in range(batch):
+        gx, gz = xqr.lsq_solve(a[s], b[s])
+        assert codes[s] == 0 and cols[s] == 0
+        assert_same(x[s], gx, f"x[{s}]")
+        assert_same(z[s], gz, f"z[{s}]")
